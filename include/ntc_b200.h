@@ -1,0 +1,213 @@
+/*
+ * ntc_b200.h — C-ABI of the B200-native hot path of arXiv 2109.09534
+ * (nonnegative tensor completion, per-mode stochastic accelerated projected
+ * gradient "S_NMC" inside the AO sweep).
+ *
+ * The reference ("ntc", /root/reference/proj/core) is a C++20 library whose
+ * hot path is called in-process; it has no FFI.  This header is the drop-in
+ * boundary a C/C++/ctypes caller binds instead of the reference's C++ API.
+ * Plain pointers and sizes only; no torch or CUDA types (streams cross as
+ * void*).  Every entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Return value: NTCB_OK (0) or an error code mirroring the C++ exception
+ *     the reference throws in the same situation; ntcb_last_error() returns
+ *     the message (same text as the reference's what()).
+ *   - Host matrices are row-major double I x R, exactly ntc::Matrix
+ *     (matrix.hpp:12-55).  On the device factors are fp32, row stride ld.
+ *   - RNG streams cross as their raw 64-bit splitmix state: the state of
+ *     ntc::RngStream (rng.hpp:13-63).  ntcb_sweep_stream_state() gives the
+ *     state of sweep_stream(seed, k, mode) (ao.cpp:65-68).
+ *   - Calls on one context are not re-entrant (like s_nmc, nmc.hpp:93-95).
+ */
+#ifndef NTC_B200_H_
+#define NTC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTCB_OK 0
+#define NTCB_EINVAL 1   /* std::invalid_argument */
+#define NTCB_ERUNTIME 2 /* std::runtime_error    */
+#define NTCB_ERANGE 3   /* std::out_of_range     */
+#define NTCB_EDOMAIN 4  /* std::domain_error     */
+#define NTCB_ECUDA 5    /* CUDA / device failure (no reference analogue) */
+
+#define NTCB_MAX_ORDER 8
+#define NTCB_MAX_RANK 64
+
+typedef struct ntcb_context ntcb_context;
+
+/* ntc::NmcConfig (nmc.hpp:13-23); validated like NmcConfig::validate
+ * (nmc.cpp:13-23).  threads/chunk are validated and otherwise ignored: the
+ * device schedule never changes results (nmc.hpp:89-92). */
+typedef struct ntcb_nmc_config {
+  double lambda;
+  double c;
+  int32_t max_inner;
+  int32_t power_iters;
+  double power_tol;
+  int32_t threads;
+  int32_t chunk;
+} ntcb_nmc_config;
+
+/* ntc::AoConfig (ao.hpp:12-29). */
+typedef struct ntcb_ao_config {
+  uint64_t rank;
+  double lambda;
+  double c;
+  int32_t max_inner;
+  int32_t power_iters;
+  double max_epochs;
+  double term_tol;
+  uint64_t seed;
+  int32_t threads;
+  int32_t chunk;
+  double power_tol;
+  int32_t eval_metrics;
+  int32_t metrics_every;
+} ntcb_ao_config;
+
+/* ntc::MetricsRecord (ao.hpp:31-37). */
+typedef struct ntcb_metrics_record {
+  double epoch;
+  double objective;
+  double rel_error;
+  double wall_seconds;
+  uint64_t entries_accessed;
+} ntcb_metrics_record;
+
+/* ntc::SweepObserver (ao.hpp:55): called after each record with the record;
+ * factors are readable through ntcb_factor_get from inside the callback. */
+typedef void (*ntcb_observer_fn)(const ntcb_metrics_record* rec, ntcb_context* ctx, void* user);
+
+/* ---- library / context ------------------------------------------------- */
+const char* ntcb_last_error(void);
+int ntcb_version(void);
+int ntcb_create(int device, ntcb_context** out);
+int ntcb_destroy(ntcb_context* ctx);
+/* Use the caller's cudaStream_t (e.g. torch.cuda.current_stream()); NULL
+ * restores the context's own stream. */
+int ntcb_set_stream(ntcb_context* ctx, void* cuda_stream);
+int ntcb_synchronize(ntcb_context* ctx);
+
+/* ---- RNG (rng.hpp:13-63, ao.cpp:65-68) — host-side helpers ------------- */
+uint64_t ntcb_rng_fork(uint64_t state, uint64_t tag);
+uint64_t ntcb_sweep_stream_state(uint64_t seed, uint64_t sweep, int mode);
+
+/* ---- tensor + mode views ------------------------------------------------
+ * Replaces ntc::SparseTensor(dims, indices, values) (sparse_tensor.cpp:24-73)
+ * followed by build_mode_views (mode_view.cpp:8-37).  indices: nnz*order
+ * 0-based coordinates, entry-major, any order; values: double (rounded to
+ * fp32 on the device, the path's arithmetic type).  Validation, canonical
+ * lexicographic sort, duplicate detection and the per-mode stable views are
+ * all built on the device; same error texts as the reference. */
+int ntcb_tensor_load(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                     const uint32_t* indices, const double* values);
+/* Same, with fp32 values (the benchmark path: no double staging). */
+int ntcb_tensor_load_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                         const uint32_t* indices, const float* values);
+/* Same, inputs already in device memory (e.g. from ntcb_synth_*). */
+int ntcb_tensor_load_device(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                            const uint32_t* d_indices, const float* d_values);
+int ntcb_tensor_info(ntcb_context* ctx, int* order, uint64_t* dims, uint64_t* nnz);
+/* ModeView export (mode_view.hpp:13-29): offsets[dims[mode]+1],
+ * others[nnz*(order-1)], values[nnz]; any pointer may be NULL. */
+int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* others,
+                     float* values);
+/* Canonical (lexicographic) COO, SparseTensor::indices()/values(). */
+int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values);
+
+/* ---- factors (FactorSet, factor_set.hpp:12-35) ------------------------- */
+/* factors/momentum: order pointers to host row-major double dims[m] x rank;
+ * momentum may be NULL (= factors).  Factors must be nonnegative. */
+int ntcb_factors_init(ntcb_context* ctx, uint64_t rank, const double* const* factors,
+                      const double* const* momentum);
+/* initial_factors(dims, rank, seed) (ao.cpp:70-73) generated on the device. */
+int ntcb_factors_random(ntcb_context* ctx, uint64_t rank, uint64_t seed);
+int ntcb_factor_set(ntcb_context* ctx, int mode, const double* a, const double* y);
+int ntcb_factor_get(ntcb_context* ctx, int mode, double* a, double* y);
+/* Device pointers of factor A (which=0) or momentum Y (which=1): fp32,
+ * dims[mode] rows, row stride *ld floats (ld >= rank, padding is zero). */
+int ntcb_factor_device_ptr(ntcb_context* ctx, int mode, int which, void** ptr, uint64_t* ld);
+
+/* ---- S_NMC (nmc.hpp:93-95, nmc.cpp:199-272) -----------------------------
+ * One call = one ntc::s_nmc(views[mode], factors, mode, a_init, cfg,
+ * RngStream(rng_state), &stats): A = Y = a_init, then max_inner inner
+ * iterations over every row (sample, gradient at Y, Hessian, 1.01 x power
+ * method, projected Nesterov step).  a_init == NULL aliases factors[mode]
+ * (as ao_ntc does, ao.cpp:123); otherwise a host double dims[mode] x rank.
+ * *entries_accessed is ADDED to (nmc.cpp:270); may be NULL. */
+int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc_config* cfg,
+               uint64_t rng_state, uint64_t* entries_accessed);
+/* Host-buffer drop-in: a_init in, updated factors[mode] (a_out) and
+ * momentum[mode] (y_out) out, all host double; H2D/D2H inside the call. */
+int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a_out,
+                    double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
+                    uint64_t* entries_accessed);
+/* Row shard [row_begin, row_end) of the same update (multi-GPU partition;
+ * rows are independent, nmc.cpp:231).  a_init aliases factors[mode].
+ * Asynchronous: errors and the count are collected by ntcb_collect(). */
+int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
+                          const ntcb_nmc_config* cfg, uint64_t rng_state);
+/* Waits for queued work; adds the entries accessed since the last collect
+ * to *entries_accessed and reports the first row failure (lowest row). */
+int ntcb_collect(ntcb_context* ctx, uint64_t* entries_accessed);
+
+/* sample_row for every row in [row_begin, row_end) of view `mode` with the
+ * row stream RngStream(rng_state).fork(l).fork(p) (nmc.cpp:236): writes
+ * pick_offsets[row_end-row_begin+1] and the picks (slice-local offsets, in
+ * draw order, nmc.cpp:44-63) to host buffers; picks may be NULL to query
+ * the total (pick_offsets[last]). */
+int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, uint64_t l,
+                     uint64_t row_begin, uint64_t row_end, uint64_t* pick_offsets,
+                     uint32_t* picks);
+
+/* ntc::sample_row(view, row, c, RngStream(row_state)) (nmc.hpp:45,
+ * nmc.cpp:110-118): one row, the stream used as is.  *count receives
+ * floor(c * n); picks (capacity >= slice length) may be NULL to query. */
+int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_t row_state,
+                    uint32_t* picks, uint64_t* count);
+
+/* ---- AO driver (ao.cpp:75-133) ----------------------------------------- */
+/* One AO iteration k: s_nmc for modes 0..N-1 with sweep_stream(seed,k,i)
+ * (Gauss-Seidel, ao.cpp:121-124).  Asynchronous; see ntcb_collect. */
+int ntcb_sweep_async(ntcb_context* ctx, uint64_t sweep, const ntcb_nmc_config* cfg,
+                     uint64_t seed);
+/* ao_ntc on the resident tensor and factors (factors are the init). */
+int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_record* history,
+                uint64_t max_history, uint64_t* n_history, ntcb_observer_fn observer,
+                void* user);
+
+/* ---- metrics (metrics.cpp:8-37) ---------------------------------------- */
+/* sse = sum_Omega (x - model)^2, sumsq = sum x^2, reg = sum_m ||U_m||_F^2. */
+int ntcb_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg);
+int ntcb_objective(ntcb_context* ctx, double lambda, double* out);
+int ntcb_relative_error(ntcb_context* ctx, double* out);
+/* masked RMSE = sqrt(sse / |Omega|). */
+int ntcb_rmse(ntcb_context* ctx, double* out);
+
+/* ---- synthetic data (BASELINE.json configs; not in the reference) ------ */
+/* Uniform unique cells + rank-`true_rank` U[0,1) CPD values + N(0,sigma^2)
+ * noise clamped at 0, generated on the device from `seed`; writes device
+ * buffers owned by the context, then loads them as the tensor. */
+int ntcb_synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                       uint64_t true_rank, double sigma, uint64_t seed);
+
+/* ---- timing hooks for bench.py ----------------------------------------- */
+/* Kernel-level timing of the last ntcb_collect window: total device ms of
+ * the update (accumulate) kernels and of the sampler kernels, and number of
+ * kernel launches, measured with CUDA events on the context stream. */
+int ntcb_profile_enable(ntcb_context* ctx, int on);
+int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms,
+                      uint64_t* launches, uint64_t* update_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NTC_B200_H_ */

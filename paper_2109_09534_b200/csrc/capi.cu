@@ -1,0 +1,733 @@
+// C-ABI of ntc-b200 (include/ntc_b200.h): context, tensor/factor residency,
+// the S_NMC call sequence, the AO driver and metrics.  Host orchestration
+// only; all arithmetic of the path runs in the kernels of sampler.cu,
+// update.cu, metrics.cu and tensor.cu.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ntcb {
+int launch_sample(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end, double c,
+                  uint64_t root, uint32_t* dbg_picks, const uint64_t* dbg_off, int direct = 0);
+int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
+                  const ntcb_nmc_config& cfg);
+void free_views(ntcb_context* ctx);
+void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                     const uint32_t* h_idx, const double* h_vals);
+void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                     const uint32_t* idx, const float* vals, bool on_device);
+void device_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg);
+void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                   uint64_t true_rank, double sigma, uint64_t seed);
+}  // namespace ntcb
+
+using namespace ntcb;
+
+namespace {
+
+thread_local std::string g_err;
+
+// Per-context host bookkeeping that does not belong in the POD context.
+struct HostState {
+  uint64_t pending_accessed = 0;
+  bool verified[NTCB_MAX_ORDER] = {};  // factor rows known nonnegative
+  std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, uint64_t> bs_cache;
+};
+std::map<const ntcb_context*, HostState> g_host;
+
+#define API_TRY try {
+#define API_CATCH                                   \
+  }                                                 \
+  catch (const ntcb::Error& e) {                    \
+    g_err = e.what();                               \
+    return e.code;                                  \
+  }                                                 \
+  catch (const std::exception& e) {                 \
+    g_err = e.what();                               \
+    return NTCB_ECUDA;                              \
+  }                                                 \
+  return NTCB_OK;
+
+void need_ctx(ntcb_context* ctx) {
+  if (!ctx) fail(NTCB_EINVAL, "ntcb: null context");
+  NTCB_CUDA(cudaSetDevice(ctx->device));
+}
+void need_tensor(ntcb_context* ctx) {
+  if (ctx->order < 2) fail(NTCB_EINVAL, "ntcb: no tensor loaded");
+}
+void need_factors(ntcb_context* ctx) {
+  need_tensor(ctx);
+  if (ctx->rank == 0 || !ctx->A[0]) fail(NTCB_EINVAL, "ntcb: no factors loaded");
+}
+
+void validate_nmc(const ntcb_nmc_config* c) {  // NmcConfig::validate, nmc.cpp:13-23
+  if (!c) fail(NTCB_EINVAL, "NmcConfig: null");
+  if (!(c->lambda > 0.0)) fail(NTCB_EINVAL, "NmcConfig: lambda must be > 0");
+  if (!(c->c > 0.0 && c->c <= 1.0)) fail(NTCB_EINVAL, "NmcConfig: c must be in (0, 1]");
+  if (c->max_inner < 0) fail(NTCB_EINVAL, "NmcConfig: max_inner must be >= 0");
+  if (c->power_iters < 1) fail(NTCB_EINVAL, "NmcConfig: power_iters must be >= 1");
+  if (!(c->power_tol > 0.0)) fail(NTCB_EINVAL, "NmcConfig: power_tol must be > 0");
+  if (c->threads < 1) fail(NTCB_EINVAL, "NmcConfig: threads must be >= 1");
+  if (c->chunk < 0) fail(NTCB_EINVAL, "NmcConfig: chunk must be >= 0");
+}
+
+// sum over rows of floor(c * n_p) (nmc.cpp:36-40) -- known before the run.
+uint64_t blocksize_sum(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, double c) {
+  auto& hs = g_host[ctx];
+  uint64_t cbits;
+  std::memcpy(&cbits, &c, 8);
+  auto key = std::make_tuple(mode, r0, r1, cbits);
+  auto it = hs.bs_cache.find(key);
+  if (it != hs.bs_cache.end()) return it->second;
+  const uint64_t* off = ctx->views[mode].h_off;
+  uint64_t s = 0;
+  for (uint64_t p = r0; p < r1; ++p) s += blocksize_for(c, off[p + 1] - off[p]);
+  hs.bs_cache[key] = s;
+  return s;
+}
+
+void prof_mark(ntcb_context* ctx, int kind) {
+  Profile& pf = ctx->prof;
+  if (!pf.on) return;
+  if (pf.n + 2 > 4096) return;
+  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], ctx->stream));
+  pf.kind[pf.n / 2] = kind;
+  pf.n += 1;
+}
+void prof_end(ntcb_context* ctx) {
+  Profile& pf = ctx->prof;
+  if (!pf.on || (pf.n & 1) == 0) return;
+  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], ctx->stream));
+  pf.n += 1;
+}
+
+// Queue one s_nmc on rows [r0, r1) of `mode` with a_init == factors[mode].
+void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
+                  const ntcb_nmc_config& cfg, uint64_t rng_state) {
+  const uint64_t ld = ctx->ld;
+  cudaStream_t st = ctx->stream;
+  if (r1 <= r0) return;
+  // A_0 = Y_0 = a_init (nmc.cpp:212-215); A already holds a_init.
+  NTCB_CUDA(cudaMemcpyAsync(ctx->Y[mode] + r0 * ld, ctx->A[mode] + r0 * ld,
+                            sizeof(float) * (r1 - r0) * ld, cudaMemcpyDeviceToDevice, st));
+  const DeviceView& v = ctx->views[mode];
+  const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
+  for (int l = 0; l < cfg.max_inner; ++l) {
+    const uint64_t root = fork64(rng_state, static_cast<uint64_t>(l));
+    if (cfg.c < 1.0 && e1 > e0) {
+      const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
+      NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), st));
+      prof_mark(ctx, 1);
+      ctx->prof.launches += launch_sample(ctx, mode, r0, r1, cfg.c, root, nullptr, nullptr);
+      prof_end(ctx);
+    }
+    prof_mark(ctx, 0);
+    const int n = launch_update(ctx, mode, r0, r1, cfg);
+    ctx->prof.launches += n;
+    ctx->prof.update_launches += n;
+    prof_end(ctx);
+  }
+  g_host[ctx].pending_accessed +=
+      static_cast<uint64_t>(cfg.max_inner) * blocksize_sum(ctx, mode, r0, r1, cfg.c);
+}
+
+// Waits and converts a device-side row failure into the reference's exception.
+void collect(ntcb_context* ctx, uint64_t* accessed) {
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  NTCB_CUDA(cudaMemcpy(ctx->h_counters, ctx->counters, 2 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost));
+  auto& hs = g_host[ctx];
+  const unsigned long long key = ctx->h_counters[1];
+  const uint64_t pend = hs.pending_accessed;
+  hs.pending_accessed = 0;
+  if (key != ~0ull) {
+    const unsigned long long reset = ~0ull;
+    NTCB_CUDA(cudaMemcpy(ctx->counters + 1, &reset, sizeof reset, cudaMemcpyHostToDevice));
+    const int mode = static_cast<int>(key >> 58);
+    const uint64_t row = (key >> 2) & ((1ull << 56) - 1);
+    const int kind = static_cast<int>(key & 3);
+    hs.verified[mode] = false;
+    if (kind == 0)
+      fail(NTCB_ERUNTIME, "s_nmc: non-finite gradient at row " + std::to_string(row + 1) +
+                              " (mode " + std::to_string(mode + 1) + ")");
+    if (kind == 1) fail(NTCB_ERUNTIME, "power_method: non-finite entries in matrix");
+    fail(NTCB_ERUNTIME, "row_step: step constant below lambda");
+  }
+  if (accessed) *accessed += pend;
+}
+
+void upload_factor(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
+  const uint64_t R = ctx->rank, ld = ctx->ld;
+  std::vector<float> tmp(rows * ld, 0.f);
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t r = 0; r < R; ++r) tmp[i * ld + r] = static_cast<float>(src[i * R + r]);
+  NTCB_CUDA(cudaMemcpyAsync(dst, tmp.data(), sizeof(float) * rows * ld, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void download_factor(ntcb_context* ctx, const float* src, double* dst, uint64_t rows) {
+  const uint64_t R = ctx->rank, ld = ctx->ld;
+  std::vector<float> tmp(rows * ld);
+  NTCB_CUDA(cudaMemcpyAsync(tmp.data(), src, sizeof(float) * rows * ld, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t r = 0; r < R; ++r) dst[i * R + r] = static_cast<double>(tmp[i * ld + r]);
+}
+
+bool all_nonneg(const double* p, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(p[i] >= 0.0)) return false;
+  return true;
+}
+
+void free_factors(ntcb_context* ctx) {
+  for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
+    if (ctx->A[m]) cudaFree(ctx->A[m]);
+    if (ctx->Y[m]) cudaFree(ctx->Y[m]);
+    ctx->A[m] = ctx->Y[m] = nullptr;
+  }
+  ctx->rank = ctx->ld = 0;
+}
+
+void alloc_factors(ntcb_context* ctx, uint64_t rank) {
+  if (rank == 0) fail(NTCB_EINVAL, "FactorSet: rank must be positive");
+  if (rank > NTCB_MAX_RANK) fail(NTCB_EINVAL, "FactorSet: rank exceeds the supported maximum (64)");
+  need_tensor(ctx);
+  free_factors(ctx);
+  ctx->rank = rank;
+  ctx->ld = (rank + 3) / 4 * 4;
+  for (int m = 0; m < ctx->order; ++m) {
+    const size_t bytes = sizeof(float) * ctx->dims[m] * ctx->ld;
+    NTCB_CUDA(cudaMalloc(&ctx->A[m], bytes));
+    NTCB_CUDA(cudaMalloc(&ctx->Y[m], bytes));
+    NTCB_CUDA(cudaMemsetAsync(ctx->A[m], 0, bytes, ctx->stream));
+    NTCB_CUDA(cudaMemsetAsync(ctx->Y[m], 0, bytes, ctx->stream));
+  }
+  for (auto& v : g_host[ctx].verified) v = false;
+}
+
+__global__ void k_uniform_factor(uint64_t root, uint64_t rows, int R, int ld, float* a, float* y) {
+  const uint64_t n = rows * R;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double v = static_cast<double>(mix64(root + (q + 1) * kGolden) >> 11) * 0x1.0p-53;
+    const uint64_t i = q / R, r = q % R;
+    a[i * ld + r] = static_cast<float>(v);
+    y[i * ld + r] = static_cast<float>(v);
+  }
+}
+
+// plateau (ao.cpp:21-26)
+bool plateau(const std::vector<ntcb_metrics_record>& h, double tol) {
+  if (h.size() < 4) return false;
+  for (size_t t = h.size() - 3; t < h.size(); ++t)
+    if (!(std::abs(h[t].rel_error - h[t - 1].rel_error) < tol)) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ntcb_last_error(void) { return g_err.c_str(); }
+int ntcb_version(void) { return 1; }
+
+int ntcb_create(int device, ntcb_context** out) {
+  API_TRY
+  if (!out) fail(NTCB_EINVAL, "ntcb_create: null out");
+  int n = 0;
+  NTCB_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) fail(NTCB_EINVAL, "ntcb_create: no such CUDA device");
+  NTCB_CUDA(cudaSetDevice(device));
+  auto* ctx = new ntcb_context();
+  ctx->device = device;
+  NTCB_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  NTCB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+  NTCB_CUDA(cudaMalloc(&ctx->counters, 2 * sizeof(unsigned long long)));
+  NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 2 * sizeof(unsigned long long)));
+  const unsigned long long init[2] = {0, ~0ull};
+  NTCB_CUDA(cudaMemcpy(ctx->counters, init, sizeof init, cudaMemcpyHostToDevice));
+  for (auto& e : ctx->prof.ev) NTCB_CUDA(cudaEventCreate(&e));
+  g_host[ctx] = HostState{};
+  *out = ctx;
+  API_CATCH
+}
+
+int ntcb_destroy(ntcb_context* ctx) {
+  API_TRY
+  if (!ctx) return NTCB_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  free_views(ctx);
+  free_factors(ctx);
+  if (ctx->red) cudaFree(ctx->red);
+  cudaFree(ctx->counters);
+  cudaFreeHost(ctx->h_counters);
+  for (auto& e : ctx->prof.ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->own_stream);
+  g_host.erase(ctx);
+  delete ctx;
+  API_CATCH
+}
+
+int ntcb_set_stream(ntcb_context* ctx, void* s) {
+  API_TRY
+  need_ctx(ctx);
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  API_CATCH
+}
+
+int ntcb_synchronize(ntcb_context* ctx) {
+  API_TRY
+  need_ctx(ctx);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_CATCH
+}
+
+uint64_t ntcb_rng_fork(uint64_t state, uint64_t tag) { return fork64(state, tag); }
+uint64_t ntcb_sweep_stream_state(uint64_t seed, uint64_t sweep, int mode) {
+  return fork64(fork64(fork64(seed, 2), sweep), static_cast<uint64_t>(mode));  // ao.cpp:65-68
+}
+
+int ntcb_tensor_load(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                     const uint32_t* indices, const double* values) {
+  API_TRY
+  need_ctx(ctx);
+  free_factors(ctx);
+  load_tensor_f64(ctx, order, dims, nnz, indices, values);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_tensor_load_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                         const uint32_t* indices, const float* values) {
+  API_TRY
+  need_ctx(ctx);
+  free_factors(ctx);
+  load_tensor_f32(ctx, order, dims, nnz, indices, values, false);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_tensor_load_device(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                            const uint32_t* d_indices, const float* d_values) {
+  API_TRY
+  need_ctx(ctx);
+  free_factors(ctx);
+  load_tensor_f32(ctx, order, dims, nnz, d_indices, d_values, true);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                       uint64_t true_rank, double sigma, uint64_t seed) {
+  API_TRY
+  need_ctx(ctx);
+  free_factors(ctx);
+  synth_uniform(ctx, order, dims, nnz, true_rank, sigma, seed);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_tensor_info(ntcb_context* ctx, int* order, uint64_t* dims, uint64_t* nnz) {
+  API_TRY
+  need_ctx(ctx);
+  if (order) *order = ctx->order;
+  if (dims)
+    for (int m = 0; m < ctx->order; ++m) dims[m] = ctx->dims[m];
+  if (nnz) *nnz = ctx->nnz;
+  API_CATCH
+}
+
+int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* others,
+                     float* values) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_export: mode out of range");
+  const DeviceView& v = ctx->views[mode];
+  const uint64_t nnz = ctx->nnz;
+  const int no = ctx->order - 1;
+  if (offsets) std::memcpy(offsets, v.h_off, sizeof(uint64_t) * (v.rows + 1));
+  if (others && nnz) {
+    std::vector<uint32_t> col(nnz);
+    for (int k = 0; k < no; ++k) {
+      NTCB_CUDA(cudaMemcpy(col.data(), v.oth[k], sizeof(uint32_t) * nnz, cudaMemcpyDeviceToHost));
+      for (uint64_t t = 0; t < nnz; ++t) others[t * no + k] = col[t];
+    }
+  }
+  if (values && nnz)
+    NTCB_CUDA(cudaMemcpy(values, v.val, sizeof(float) * nnz, cudaMemcpyDeviceToHost));
+  API_CATCH
+}
+
+int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  // the mode-0 view IS the canonical lexicographic order (mode_view.cpp:5-7)
+  const DeviceView& v = ctx->views[0];
+  const uint64_t nnz = ctx->nnz;
+  const int N = ctx->order;
+  if (indices && nnz) {
+    std::vector<uint32_t> col(nnz);
+    for (int k = 0; k < N - 1; ++k) {
+      NTCB_CUDA(cudaMemcpy(col.data(), v.oth[k], sizeof(uint32_t) * nnz, cudaMemcpyDeviceToHost));
+      for (uint64_t t = 0; t < nnz; ++t) indices[t * N + k + 1] = col[t];
+    }
+    for (uint64_t p = 0; p < v.rows; ++p)
+      for (uint64_t t = v.h_off[p]; t < v.h_off[p + 1]; ++t) indices[t * N] = static_cast<uint32_t>(p);
+  }
+  if (values && nnz)
+    NTCB_CUDA(cudaMemcpy(values, v.val, sizeof(float) * nnz, cudaMemcpyDeviceToHost));
+  API_CATCH
+}
+
+int ntcb_factors_init(ntcb_context* ctx, uint64_t rank, const double* const* factors,
+                      const double* const* momentum) {
+  API_TRY
+  need_ctx(ctx);
+  alloc_factors(ctx, rank);
+  auto& hs = g_host[ctx];
+  for (int m = 0; m < ctx->order; ++m) {
+    upload_factor(ctx, ctx->A[m], factors[m], ctx->dims[m]);
+    upload_factor(ctx, ctx->Y[m], momentum ? momentum[m] : factors[m], ctx->dims[m]);
+    hs.verified[m] = all_nonneg(factors[m], ctx->dims[m] * rank);
+  }
+  API_CATCH
+}
+
+int ntcb_factors_random(ntcb_context* ctx, uint64_t rank, uint64_t seed) {
+  API_TRY
+  need_ctx(ctx);
+  alloc_factors(ctx, rank);
+  const uint64_t base = fork64(seed, 1);  // initial_factors, ao.cpp:70-73
+  for (int m = 0; m < ctx->order; ++m) {
+    const uint64_t n = ctx->dims[m] * rank;
+    const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096));
+    k_uniform_factor<<<g, 256, 0, ctx->stream>>>(fork64(base, m), ctx->dims[m],
+                                                 static_cast<int>(rank), static_cast<int>(ctx->ld),
+                                                 ctx->A[m], ctx->Y[m]);
+    NTCB_CUDA(cudaGetLastError());
+    g_host[ctx].verified[m] = true;
+  }
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_CATCH
+}
+
+int ntcb_factor_set(ntcb_context* ctx, int mode, const double* a, const double* y) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_set: mode out of range");
+  if (a) {
+    upload_factor(ctx, ctx->A[mode], a, ctx->dims[mode]);
+    g_host[ctx].verified[mode] = all_nonneg(a, ctx->dims[mode] * ctx->rank);
+  }
+  if (y) upload_factor(ctx, ctx->Y[mode], y, ctx->dims[mode]);
+  API_CATCH
+}
+
+int ntcb_factor_get(ntcb_context* ctx, int mode, double* a, double* y) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_get: mode out of range");
+  if (a) download_factor(ctx, ctx->A[mode], a, ctx->dims[mode]);
+  if (y) download_factor(ctx, ctx->Y[mode], y, ctx->dims[mode]);
+  API_CATCH
+}
+
+int ntcb_factor_device_ptr(ntcb_context* ctx, int mode, int which, void** ptr, uint64_t* ld) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_device_ptr: mode out of range");
+  if (ptr) *ptr = which ? ctx->Y[mode] : ctx->A[mode];
+  if (ld) *ld = ctx->ld;
+  API_CATCH
+}
+
+int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc_config* cfg,
+               uint64_t rng_state, uint64_t* entries_accessed) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  auto& hs = g_host[ctx];
+  if (a_init) {
+    if (!all_nonneg(a_init, ctx->dims[mode] * ctx->rank))
+      fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+    upload_factor(ctx, ctx->A[mode], a_init, ctx->dims[mode]);
+    hs.verified[mode] = true;
+  } else if (!hs.verified[mode]) {
+    fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+  }
+  collect(ctx, nullptr);  // drain anything queued before
+  enqueue_snmc(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state);
+  collect(ctx, entries_accessed);
+  API_CATCH
+}
+
+int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a_out,
+                    double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
+                    uint64_t* entries_accessed) {
+  int rc = ntcb_s_nmc(ctx, mode, a_init, cfg, rng_state, entries_accessed);
+  if (rc) return rc;
+  return ntcb_factor_get(ctx, mode, a_out, y_out);
+}
+
+int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
+                          const ntcb_nmc_config* cfg, uint64_t rng_state) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  if (row_begin > row_end || row_end > ctx->dims[mode])
+    fail(NTCB_ERANGE, "s_nmc: row range out of bounds");
+  if (!g_host[ctx].verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+  enqueue_snmc(ctx, mode, row_begin, row_end, *cfg, rng_state);
+  API_CATCH
+}
+
+int ntcb_collect(ntcb_context* ctx, uint64_t* entries_accessed) {
+  API_TRY
+  need_ctx(ctx);
+  collect(ctx, entries_accessed);
+  API_CATCH
+}
+
+int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, uint64_t l,
+                     uint64_t row_begin, uint64_t row_end, uint64_t* pick_offsets,
+                     uint32_t* picks) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "sample_rows: mode out of range");
+  if (row_begin > row_end || row_end > ctx->dims[mode])
+    fail(NTCB_ERANGE, "sample_row: row out of range");
+  if (!(c > 0.0 && c <= 1.0)) fail(NTCB_EINVAL, "sample_row: c must be in (0, 1]");
+  const uint64_t* off = ctx->views[mode].h_off;
+  const uint64_t rows = row_end - row_begin;
+  std::vector<uint64_t> po(rows + 1, 0);
+  for (uint64_t i = 0; i < rows; ++i)
+    po[i + 1] = po[i] + blocksize_for(c, off[row_begin + i + 1] - off[row_begin + i]);
+  if (pick_offsets) std::memcpy(pick_offsets, po.data(), sizeof(uint64_t) * (rows + 1));
+  if (!picks || po[rows] == 0) return NTCB_OK;
+  uint64_t* d_po = nullptr;
+  uint32_t* d_pk = nullptr;
+  NTCB_CUDA(cudaMalloc(&d_po, sizeof(uint64_t) * (rows + 1)));
+  NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * po[rows]));
+  NTCB_CUDA(cudaMemcpy(d_po, po.data(), sizeof(uint64_t) * (rows + 1), cudaMemcpyHostToDevice));
+  const uint64_t e0 = off[row_begin], e1 = off[row_end];
+  if (e1 > e0) {
+    const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
+    NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
+  }
+  launch_sample(ctx, mode, row_begin, row_end, c, fork64(rng_state, l), d_pk, d_po);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  NTCB_CUDA(cudaMemcpy(picks, d_pk, sizeof(uint32_t) * po[rows], cudaMemcpyDeviceToHost));
+  cudaFree(d_po);
+  cudaFree(d_pk);
+  API_CATCH
+}
+
+int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_t row_state,
+                    uint32_t* picks, uint64_t* count) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "sample_row: mode out of range");
+  if (row >= ctx->dims[mode]) fail(NTCB_ERANGE, "sample_row: row out of range");
+  if (!(c > 0.0 && c <= 1.0)) fail(NTCB_EINVAL, "sample_row: c must be in (0, 1]");
+  const uint64_t* off = ctx->views[mode].h_off;
+  const uint64_t b = blocksize_for(c, off[row + 1] - off[row]);
+  if (count) *count = b;
+  if (!picks || b == 0) return NTCB_OK;
+  uint64_t* d_po = nullptr;
+  uint32_t* d_pk = nullptr;
+  const uint64_t po[2] = {0, b};
+  NTCB_CUDA(cudaMalloc(&d_po, sizeof po));
+  NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * b));
+  NTCB_CUDA(cudaMemcpy(d_po, po, sizeof po, cudaMemcpyHostToDevice));
+  const uint64_t e0 = off[row], e1 = off[row + 1];
+  const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
+  NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
+  launch_sample(ctx, mode, row, row + 1, c, row_state, d_pk, d_po, 1);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  NTCB_CUDA(cudaMemcpy(picks, d_pk, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost));
+  cudaFree(d_po);
+  cudaFree(d_pk);
+  API_CATCH
+}
+
+int ntcb_sweep_async(ntcb_context* ctx, uint64_t sweep, const ntcb_nmc_config* cfg, uint64_t seed) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_factors(ctx);
+  for (int i = 0; i < ctx->order; ++i) {
+    if (!g_host[ctx].verified[i]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+    enqueue_snmc(ctx, i, 0, ctx->dims[i], *cfg, ntcb_sweep_stream_state(seed, sweep, i));
+  }
+  API_CATCH
+}
+
+int ntcb_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  collect(ctx, nullptr);
+  double a, b, c;
+  device_metrics(ctx, &a, &b, &c);
+  if (sse) *sse = a;
+  if (sumsq) *sumsq = b;
+  if (reg) *reg = c;
+  API_CATCH
+}
+
+int ntcb_objective(ntcb_context* ctx, double lambda, double* out) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (lambda < 0.0) fail(NTCB_EINVAL, "objective: lambda must be >= 0");
+  double sse, sx, reg;
+  device_metrics(ctx, &sse, &sx, &reg);
+  *out = 0.5 * sse + 0.5 * lambda * reg;  // metrics.cpp:8-21
+  API_CATCH
+}
+
+int ntcb_relative_error(ntcb_context* ctx, double* out) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  double sse, sx, reg;
+  device_metrics(ctx, &sse, &sx, &reg);
+  if (sx == 0.0) fail(NTCB_EDOMAIN, "relative_error: all observed values are zero");
+  *out = std::sqrt(sse) / std::sqrt(sx);  // metrics.cpp:23-37
+  API_CATCH
+}
+
+int ntcb_rmse(ntcb_context* ctx, double* out) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (ctx->nnz == 0) fail(NTCB_EDOMAIN, "rmse: empty observation set");
+  double sse, sx, reg;
+  device_metrics(ctx, &sse, &sx, &reg);
+  *out = std::sqrt(sse / static_cast<double>(ctx->nnz));
+  API_CATCH
+}
+
+int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_record* history,
+                uint64_t max_history, uint64_t* n_history, ntcb_observer_fn observer, void* user) {
+  API_TRY
+  need_ctx(ctx);
+  if (!cfg) fail(NTCB_EINVAL, "AoConfig: null");
+  // AoConfig::validate (ao.cpp:30-38)
+  if (cfg->rank == 0) fail(NTCB_EINVAL, "AoConfig: rank must be positive");
+  if (!(cfg->max_epochs >= 0.0)) fail(NTCB_EINVAL, "AoConfig: max_epochs must be >= 0");
+  if (!(cfg->term_tol >= 0.0)) fail(NTCB_EINVAL, "AoConfig: term_tol must be >= 0");
+  if (cfg->metrics_every < 1) fail(NTCB_EINVAL, "AoConfig: metrics_every must be >= 1");
+  ntcb_nmc_config n{cfg->lambda, cfg->c, cfg->max_inner, cfg->power_iters, cfg->power_tol,
+                    cfg->threads, cfg->chunk};
+  validate_nmc(&n);
+  need_factors(ctx);
+  if (ctx->rank != cfg->rank) fail(NTCB_EINVAL, "ao_ntc: init rank differs from configured rank");
+  auto& hs = g_host[ctx];
+  for (int m = 0; m < ctx->order; ++m)
+    if (!hs.verified[m]) fail(NTCB_EINVAL, "ao_ntc: init factors must be nonnegative");
+  collect(ctx, nullptr);
+
+  std::vector<ntcb_metrics_record> hist;
+  uint64_t accessed = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto push = [&]() {
+    ntcb_metrics_record r{};
+    r.entries_accessed = accessed;
+    if (ctx->nnz == 0) fail(NTCB_EINVAL, "epoch_fraction: empty observation set");
+    r.epoch = static_cast<double>(accessed) / static_cast<double>(ctx->nnz);
+    r.wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r.objective = std::nan("");
+    r.rel_error = std::nan("");
+    if (cfg->eval_metrics) {
+      double sse, sx, reg;
+      device_metrics(ctx, &sse, &sx, &reg);
+      r.objective = 0.5 * sse + 0.5 * cfg->lambda * reg;
+      if (sx == 0.0) fail(NTCB_EDOMAIN, "relative_error: all observed values are zero");
+      r.rel_error = std::sqrt(sse) / std::sqrt(sx);
+      if (!std::isfinite(r.objective)) fail(NTCB_ERUNTIME, "ao_ntc: objective diverged (non-finite)");
+    }
+    hist.push_back(r);
+    if (observer) observer(&r, ctx, user);
+  };
+  push();
+  bool last_recorded = true;
+  for (uint64_t k = 0;; ++k) {
+    if (static_cast<double>(accessed) / static_cast<double>(ctx->nnz) >= cfg->max_epochs) break;
+    if (plateau(hist, cfg->term_tol)) break;
+    uint64_t st = 0;
+    for (int i = 0; i < ctx->order; ++i)
+      enqueue_snmc(ctx, i, 0, ctx->dims[i], n, ntcb_sweep_stream_state(cfg->seed, k, i));
+    collect(ctx, &st);
+    if (st == 0) break;
+    accessed += st;
+    last_recorded = ((k + 1) % static_cast<uint64_t>(cfg->metrics_every) == 0);
+    if (last_recorded) push();
+  }
+  if (!last_recorded) push();
+  if (n_history) *n_history = hist.size();
+  if (history)
+    for (uint64_t i = 0; i < hist.size() && i < max_history; ++i) history[i] = hist[i];
+  API_CATCH
+}
+
+int ntcb_profile_enable(ntcb_context* ctx, int on) {
+  API_TRY
+  need_ctx(ctx);
+  ctx->prof.on = on != 0;
+  ctx->prof.n = 0;
+  ctx->prof.launches = 0;
+  ctx->prof.update_launches = 0;
+  API_CATCH
+}
+
+int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms, uint64_t* launches,
+                      uint64_t* update_launches) {
+  API_TRY
+  need_ctx(ctx);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  Profile& pf = ctx->prof;
+  double u = 0.0, s = 0.0;
+  for (int i = 0; i + 1 < pf.n; i += 2) {
+    float ms = 0.f;
+    NTCB_CUDA(cudaEventElapsedTime(&ms, pf.ev[i], pf.ev[i + 1]));
+    if (pf.kind[i / 2] == 0)
+      u += ms;
+    else
+      s += ms;
+  }
+  if (update_ms) *update_ms = u;
+  if (sample_ms) *sample_ms = s;
+  if (launches) *launches = pf.launches;
+  if (update_launches) *update_launches = pf.update_launches;
+  pf.n = 0;
+  pf.launches = 0;
+  pf.update_launches = 0;
+  API_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Internal definitions shared by the ntc-b200 CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "ntc_b200.h"
+
+namespace ntcb {
+
+// ---------------------------------------------------------------------------
+// Errors.  Each C-ABI entry point catches these and maps them to the code of
+// the exception the reference throws in the same situation.
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define NTCB_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      ::ntcb::fail(NTCB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Splitmix64 stream, bit-identical to ntc::RngStream (rng.hpp:13-63).
+// ---------------------------------------------------------------------------
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.hpp:55-59
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t fork64(uint64_t s, uint64_t tag) {  // rng.hpp:18-20
+  return mix64(s ^ (kGolden * (tag + 1)));
+}
+
+// floor(c * n) in double, clamped to n; c >= 1 -> n (nmc.cpp:36-40).
+__host__ __device__ __forceinline__ uint64_t blocksize_for(double c, uint64_t n) {
+  if (c >= 1.0) return n;
+  const uint64_t b = static_cast<uint64_t>(floor(c * static_cast<double>(n)));
+  return b > n ? n : b;
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident mode view: CSR over the rows of the mode-m unfolding.
+// Structure-of-arrays so that a CTA streams a slice with fully coalesced
+// (and 128-bit vectorisable) loads:
+//   off[rows+1]           slice p = entries [off[p], off[p+1])
+//   oth[k][nnz]           k-th non-mode coordinate (ascending mode order)
+//   val[nnz]              fp32 value
+// Entry order inside a slice is the reference's (mode_view.cpp:5-7):
+// lexicographic in the remaining coordinates.
+// ---------------------------------------------------------------------------
+struct DeviceView {
+  uint64_t rows = 0;
+  uint64_t max_slice = 0;
+  uint64_t* off = nullptr;
+  uint32_t* oth[NTCB_MAX_ORDER - 1] = {};
+  float* val = nullptr;
+  uint64_t* h_off = nullptr;  // host copy of the offsets (shard planning, blocksizes)
+};
+
+// Kernel-argument bundle describing the factor matrices.
+struct FactorArgs {
+  const float* U[NTCB_MAX_ORDER];  // factor m: dims[m] x ld, fp32
+  int order;
+  int mode;
+  int rank;
+  int ld;
+};
+
+// Launch statistics gathered when profiling is on.
+struct Profile {
+  bool on = false;
+  cudaEvent_t ev[4096];
+  int kind[2048];
+  int n = 0;
+  uint64_t launches = 0;
+  uint64_t update_launches = 0;
+};
+
+}  // namespace ntcb
+
+// The opaque context behind ntcb_context*.
+struct ntcb_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+
+  // tensor
+  int order = 0;
+  uint64_t dims[NTCB_MAX_ORDER] = {};
+  uint64_t nnz = 0;
+  ntcb::DeviceView views[NTCB_MAX_ORDER];
+
+  // factors
+  uint64_t rank = 0;
+  uint64_t ld = 0;
+  float* A[NTCB_MAX_ORDER] = {};
+  float* Y[NTCB_MAX_ORDER] = {};
+
+  // scratch
+  uint32_t* mask = nullptr;  // one bit per view entry (sampled set)
+  uint64_t mask_words = 0;
+  uint32_t* perm_scratch = nullptr;  // per-entry Fisher-Yates scratch for slices too big for smem
+  uint64_t perm_scratch_n = 0;
+  unsigned long long* counters = nullptr;  // [0] entries accessed, [1] first error key
+  unsigned long long* h_counters = nullptr;  // pinned mirror
+  double* red = nullptr;  // metrics partials
+  uint64_t red_n = 0;
+  int error_mode = -1;    // mode of the queued updates (error text)
+
+  // synthetic data buffers (owned)
+  ntcb::Profile prof;
+};

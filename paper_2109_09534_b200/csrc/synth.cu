@@ -1,0 +1,201 @@
+// Synthetic tensors of the BASELINE.json shapes, generated on the device.
+// (Not part of the reference: its synth_generate (synth.cpp:84-145) cannot
+// express exact-count uniform sampling at these sizes.)
+//
+// Uniform configs: candidate cell j has coordinates
+//   i_m = hi32( hi32(mix(S_mask + (j*N + m + 1) G)) * dims[m] )
+// with S_mask = fork(fork(seed, 5), 0); candidates are taken in j order and a
+// cell already seen is redrawn (= skipped), until nnz unique cells exist.
+// Truth factors U_m[i, r] = next_double of fork(fork(seed, 4), m) at index
+// i*R + r (row-major, as FactorSet::random_uniform, factor_set.cpp:18-27);
+// value = sum_r prod_m U_m[i_m, r] + sigma * gauss_j, clamped at 0, where
+// gauss_j is the reference's Box-Muller (rng.hpp:49-53) on fork(fork(seed,6), j).
+// Tags 4..6 follow synth.cpp:16-18.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ntcb {
+
+void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                     const uint32_t* idx, const float* vals, bool on_device);
+
+namespace {
+
+template <class T>
+struct Buf {
+  T* p = nullptr;
+  explicit Buf(size_t n) {
+    if (n) NTCB_CUDA(cudaMalloc(&p, sizeof(T) * n));
+  }
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct Dims {
+  uint64_t d[NTCB_MAX_ORDER];
+  int shift[NTCB_MAX_ORDER];
+  int order;
+};
+
+__device__ __forceinline__ uint32_t coord_of(uint64_t s_mask, uint64_t j, int m, int order,
+                                             uint64_t dim) {
+  const uint64_t u = mix64(s_mask + (j * order + m + 1) * kGolden);
+  return static_cast<uint32_t>(((u >> 32) * dim) >> 32);
+}
+
+__global__ void k_candidates(uint64_t s_mask, uint64_t M, Dims d, uint64_t* key, uint32_t* jj) {
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < M;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t k = 0;
+    for (int m = 0; m < d.order; ++m)
+      k |= static_cast<uint64_t>(coord_of(s_mask, j, m, d.order, d.d[m])) << d.shift[m];
+    key[j] = k;
+    jj[j] = static_cast<uint32_t>(j);
+  }
+}
+
+// first occurrence of each cell (the sort is stable, so j ascends in a run)
+__global__ void k_first(const uint64_t* skey, const uint32_t* sj, uint64_t M, uint32_t* keep_j,
+                        unsigned long long* count) {
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < M;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const bool first = t == 0 || skey[t] != skey[t - 1];
+    keep_j[t] = first ? sj[t] : 0xffffffffu;
+    if (first) atomicAdd(count, 1ull);
+  }
+}
+
+__global__ void k_truth(uint64_t root, uint64_t n, double* out) {
+  // out[q] = q-th next_double of stream `root`
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[q] = static_cast<double>(mix64(root + (q + 1) * kGolden) >> 11) * 0x1.0p-53;
+}
+
+__global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d, int R,
+                       const double* const* truth, uint64_t noise_root, double sigma,
+                       uint32_t* idx, float* vals) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t j = js[e];
+    uint32_t ix[NTCB_MAX_ORDER];
+    for (int m = 0; m < d.order; ++m) {
+      ix[m] = coord_of(s_mask, j, m, d.order, d.d[m]);
+      idx[e * d.order + m] = ix[m];
+    }
+    double model = 0.0;
+    for (int r = 0; r < R; ++r) {
+      double prod = 1.0;
+      for (int m = 0; m < d.order; ++m) prod *= truth[m][static_cast<uint64_t>(ix[m]) * R + r];
+      model += prod;
+    }
+    double v = model;
+    if (sigma > 0.0) {
+      uint64_t s = fork64(noise_root, j);
+      s += kGolden;
+      const double u1 = static_cast<double>((mix64(s) >> 11) + 1) * 0x1.0p-53;
+      s += kGolden;
+      const double u2 = static_cast<double>(mix64(s) >> 11) * 0x1.0p-53;
+      v += sigma * sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+    }
+    vals[e] = static_cast<float>(v > 0.0 ? v : 0.0);
+  }
+}
+
+unsigned grid_of(uint64_t n, int sms) {
+  uint64_t g = (n + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(g, cap)));
+}
+
+}  // namespace
+
+void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                   uint64_t true_rank, double sigma, uint64_t seed) {
+  if (order < 2 || order > NTCB_MAX_ORDER) fail(NTCB_EINVAL, "synth: order must be in [2, 8]");
+  Dims d{};
+  d.order = order;
+  int bits = 0;
+  long double cells = 1;
+  for (int m = order - 1; m >= 0; --m) {
+    if (dims[m] == 0 || dims[m] > (1ull << 32)) fail(NTCB_EINVAL, "synth: bad dimension");
+    d.d[m] = dims[m];
+    int b = 1;
+    while (b < 64 && (dims[m] - 1) >> b) ++b;
+    d.shift[m] = bits;
+    bits += b;
+    cells *= static_cast<long double>(dims[m]);
+  }
+  if (bits > 64) fail(NTCB_EINVAL, "synth: packed cell key exceeds 64 bits");
+  if (static_cast<long double>(nnz) > 0.5L * cells)
+    fail(NTCB_EINVAL, "synth: nnz exceeds half the cell space");
+  if (true_rank == 0 || true_rank > 256) fail(NTCB_EINVAL, "synth: bad true rank");
+  cudaStream_t st = ctx->stream;
+  const int sms = ctx->sm_count;
+  const uint64_t s_mask = fork64(fork64(seed, 5), 0);
+  const uint64_t noise_root = fork64(seed, 6);
+
+  uint64_t M = nnz + std::max<uint64_t>(nnz / 256, 4096);
+  Buf<uint32_t> chosen(nnz);
+  for (int attempt = 0;; ++attempt) {
+    if (M >= (1ull << 32)) fail(NTCB_EINVAL, "synth: too many candidates");
+    Buf<uint64_t> key(M), key2(M);
+    Buf<uint32_t> jj(M), jj2(M);
+    k_candidates<<<grid_of(M, sms), 256, 0, st>>>(s_mask, M, d, key.p, jj.p);
+    NTCB_CUDA(cudaGetLastError());
+    cub::DoubleBuffer<uint64_t> dk(key.p, key2.p);
+    cub::DoubleBuffer<uint32_t> dv(jj.p, jj2.p);
+    size_t tmp = 0;
+    NTCB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, static_cast<int64_t>(M), 0, bits, st));
+    Buf<unsigned char> t(tmp);
+    NTCB_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, dk, dv, static_cast<int64_t>(M), 0, bits, st));
+    Buf<unsigned long long> cnt(1);
+    NTCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+    // keep_j reuses the idle u32 buffer
+    uint32_t* keep = dv.Current() == jj.p ? jj2.p : jj.p;
+    k_first<<<grid_of(M, sms), 256, 0, st>>>(dk.Current(), dv.Current(), M, keep, cnt.p);
+    NTCB_CUDA(cudaGetLastError());
+    unsigned long long uniq = 0;
+    NTCB_CUDA(cudaMemcpyAsync(&uniq, cnt.p, sizeof uniq, cudaMemcpyDeviceToHost, st));
+    NTCB_CUDA(cudaStreamSynchronize(st));
+    if (uniq < nnz) {
+      M = M + (nnz - uniq) * 2 + 4096;
+      continue;
+    }
+    // ascending j; skipped entries carry 0xffffffff and sort last
+    uint32_t* other = dv.Current();
+    size_t tmp2 = 0;
+    NTCB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp2, keep, other, static_cast<int64_t>(M), 0, 32, st));
+    Buf<unsigned char> t2(tmp2);
+    NTCB_CUDA(cub::DeviceRadixSort::SortKeys(t2.p, tmp2, keep, other, static_cast<int64_t>(M), 0, 32, st));
+    NTCB_CUDA(cudaMemcpyAsync(chosen.p, other, sizeof(uint32_t) * nnz, cudaMemcpyDeviceToDevice, st));
+    NTCB_CUDA(cudaStreamSynchronize(st));
+    break;
+  }
+
+  const int R = static_cast<int>(true_rank);
+  std::vector<double*> truth(order, nullptr);
+  for (int m = 0; m < order; ++m) {
+    NTCB_CUDA(cudaMalloc(&truth[m], sizeof(double) * dims[m] * R));
+    k_truth<<<grid_of(dims[m] * R, sms), 256, 0, st>>>(fork64(fork64(seed, 4), m), dims[m] * R,
+                                                       truth[m]);
+    NTCB_CUDA(cudaGetLastError());
+  }
+  Buf<double*> dtruth(NTCB_MAX_ORDER);
+  NTCB_CUDA(cudaMemcpyAsync(dtruth.p, truth.data(), sizeof(double*) * order, cudaMemcpyHostToDevice, st));
+  Buf<uint32_t> idx(nnz * order);
+  Buf<float> vals(nnz);
+  k_emit<<<grid_of(nnz, sms), 256, 0, st>>>(chosen.p, nnz, s_mask, d, R, dtruth.p, noise_root,
+                                            sigma, idx.p, vals.p);
+  NTCB_CUDA(cudaGetLastError());
+  NTCB_CUDA(cudaStreamSynchronize(st));
+  for (double* p : truth) cudaFree(p);
+  load_tensor_f32(ctx, order, dims, nnz, idx.p, vals.p, true);
+}
+
+}  // namespace ntcb

@@ -1,0 +1,396 @@
+"""GPU parity: the CUDA path (through the C-ABI, libntcb.so) against the
+reference's own outputs (golden vectors made from the compiled reference) and
+the bit-exact C restatement (oracle/), on identical seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * sampled index sets / picks and the nonzero permutation: bit-exact;
+  * entries_accessed, epochs: exact;
+  * factors (fp32 device vs fp64 reference): relative Frobenius error
+    <= TOL = 1e-4 per mode update / per AO iteration; metrics <= 1e-5.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def _split(flat, dims, R):
+    out, pos = [], 0
+    for d in dims:
+        out.append(flat[pos: pos + d * R].reshape(d, R).copy())
+        pos += d * R
+    return out
+
+
+@pytest.fixture(scope="module")
+def ntc(cuda_ok):
+    import paper_2109_09534_b200 as P
+    return P
+
+
+def ctx_for(ntc, dims, idx, vals):
+    c = ntc.Context(0)
+    c.load(dims, idx, vals)
+    return c
+
+
+# ---------------------------------------------------------------- tensor / views
+def test_views_bit_exact(ntc, golden):
+    for t, N in (("t1", 3), ("t4", 4)):
+        dims = [int(d) for d in golden[f"{t}_dims"]]
+        c = ctx_for(ntc, dims, golden[f"{t}_idx"], golden[f"{t}_vals"])
+        for m in range(N):
+            off, oth, val = c.view(m)
+            np.testing.assert_array_equal(off, golden[f"{t}_view{m}_off"])
+            np.testing.assert_array_equal(oth, golden[f"{t}_view{m}_oth"])
+            np.testing.assert_array_equal(val, golden[f"{t}_view{m}_val"].astype(np.float32))
+    c = ctx_for(ntc, [int(d) for d in golden["t1_dims"]], golden["t1_idx"], golden["t1_vals"])
+    ci, cv = c.canonical()
+    np.testing.assert_array_equal(ci, golden["t1_canon_idx"])
+    np.testing.assert_array_equal(cv, golden["t1_canon_vals"].astype(np.float32))
+
+
+def test_views_bit_exact_large(ntc, orc):
+    rng = np.random.default_rng(5)
+    dims = [300, 257, 1000]
+    nnz = 400_000
+    cells = rng.choice(int(np.prod(dims)), nnz, replace=False)
+    idx = np.stack(np.unravel_index(cells, dims), 1).astype(np.uint32)
+    vals = rng.random(nnz).astype(np.float32)
+    c = ctx_for(ntc, dims, idx, vals)
+    ci, cv = orc.canonicalize(dims, idx, vals.astype(np.float64))
+    gi, gv = c.canonical()
+    np.testing.assert_array_equal(gi, ci)
+    for m in range(3):
+        off, oth, val = orc.build_view(dims, ci, cv, m)
+        goff, goth, gval = c.view(m)
+        np.testing.assert_array_equal(goff, off)
+        np.testing.assert_array_equal(goth, oth)
+        np.testing.assert_array_equal(gval, val.astype(np.float32))
+
+
+def test_tensor_rejections_match_reference(ntc):
+    c = ntc.Context(0)
+    cases = [
+        ([2, 2, 2], [[0, 1, 0], [1, 1, 1], [0, 1, 0]], [1.0, 2.0, 3.0],
+         "SparseTensor: duplicate index (1,2,1)"),
+        ([2, 2], [[0, 1], [2, 0]], [1.0, 2.0], "SparseTensor: index out of bounds at entry 1"),
+        ([2, 2], [[0, 1], [1, 1]], [1.0, -2.0], "SparseTensor: negative value at entry 1"),
+        ([2, 2], [[0, 1]], [np.nan], "SparseTensor: non-finite value at entry 0"),
+        ([3], [[0]], [1.0], "SparseTensor: order must be >= 2"),
+        ([3, 0], [[0, 0]], [1.0], "SparseTensor: dimensions must be positive"),
+    ]
+    for dims, idx, vals, msg in cases:
+        with pytest.raises(ValueError) as e:
+            c.load(dims, np.array(idx, np.uint32), np.array(vals, np.float64))
+        assert str(e.value) == msg
+        if O.ref_available():
+            with pytest.raises(ValueError) as e2:
+                O.RefProblem(dims, np.array(idx, np.uint32), np.array(vals, np.float64))
+            assert str(e2.value) == msg
+
+
+# ---------------------------------------------------------------- sampling
+def test_sample_row_kat(ntc, golden):
+    idx = np.array([[0, j] for j in range(40)], np.uint32)
+    t = ntc.SparseTensor([1, 40], idx, np.ones(40))
+    got = ntc.sample_row(t, 0, 0, 0.4, ntc.RngStream(42))
+    np.testing.assert_array_equal(got, golden["sample_1x40_c04_s42"])
+    assert list(got) == [29, 7, 12, 15, 5, 35, 13, 33, 18, 28, 16, 25, 26, 27, 31, 20]
+    np.testing.assert_array_equal(ntc.sample_row(t, 0, 0, 0.4, ntc.RngStream(43)),
+                                  golden["sample_1x40_c04_s43"])
+    np.testing.assert_array_equal(ntc.sample_row(t, 0, 0, 1.0, ntc.RngStream(1)), np.arange(40))
+    with pytest.raises(IndexError):
+        ntc.sample_row(t, 0, 7, 0.5, ntc.RngStream(1))
+    with pytest.raises(ValueError):
+        ntc.sample_row(t, 0, 0, 0.0, ntc.RngStream(1))
+
+
+def test_sampler_all_rows_bit_exact(ntc, golden, orc):
+    dims = [int(d) for d in golden["t1_dims"]]
+    c = ctx_for(ntc, dims, golden["t1_idx"], golden["t1_vals"])
+    for cf in (0.5, 0.3, 0.05):
+        for m in range(3):
+            picks, offs = [], [0]
+            for l in range(2):
+                po, pk = c.sample_rows(m, cf, orc.sweep_state(11, 0, m), l)
+                picks.append(pk)
+                offs.extend((offs[-1] + po[1:]).tolist())
+            np.testing.assert_array_equal(np.concatenate(picks), golden[f"t1_picks_c{cf}_m{m}"])
+            np.testing.assert_array_equal(np.array(offs, np.uint64), golden[f"t1_pickoff_c{cf}_m{m}"])
+
+
+@pytest.mark.parametrize("slice_len", [37, 1000, 23000, 70000])
+def test_sampler_long_slices_bit_exact(ntc, orc, slice_len):
+    """Slices in shared memory (u16/u32 perm) and beyond it (global scratch)."""
+    rows = 6
+    dims = [rows, slice_len]
+    idx = np.array([[p, j] for p in range(rows) for j in range(slice_len)], np.uint32)
+    keep = np.random.default_rng(slice_len).random(len(idx)) < 0.9
+    idx = idx[keep]
+    vals = np.ones(len(idx), np.float32)
+    c = ctx_for(ntc, dims, idx, vals)
+    off = c.view(0)[0]
+    for cf in (0.5, 0.97, 0.013):
+        st = 0x1234 + slice_len
+        po, pk = c.sample_rows(0, cf, st, 1)
+        for p in range(rows):
+            want = orc.sample_row(int(off[p + 1] - off[p]), cf, orc.fork(orc.fork(st, 1), p))
+            np.testing.assert_array_equal(pk[po[p]:po[p + 1]], want)
+
+
+# ---------------------------------------------------------------- s_nmc
+@pytest.mark.parametrize("tag,c,mi", [("c05_i2", 0.5, 2), ("c1_i1", 1.0, 1), ("c03_i3", 0.3, 3)])
+def test_s_nmc_matches_reference(ntc, golden, orc, tag, c, mi):
+    dims = [int(d) for d in golden["t1_dims"]]
+    R = 5
+    ctx = ctx_for(ntc, dims, golden["t1_idx"], golden["t1_vals"])
+    ctx.set_factors(R, _split(golden["t1_init"], dims, R))
+    cfg = ntc.NmcConfig(lambda_=1e-3, c=c, max_inner=mi)
+    want = golden[f"t1_snmc_{tag}"]
+    pos, accs = 0, []
+    worst = 0.0
+    for k in range(2):
+        for m in range(3):
+            # teacher forcing: start every mode update from the reference's state
+            accs.append(ctx.s_nmc(m, cfg, orc.sweep_state(11, k, m)))
+            a, y = ctx.get_factor(m)
+            n = dims[m] * R
+            wa, wy = want[pos: pos + n].reshape(dims[m], R), want[pos + n: pos + 2 * n].reshape(dims[m], R)
+            worst = max(worst, rel(a, wa), rel(y, wy))
+            assert rel(a, wa) <= TOL and rel(y, wy) <= TOL, (k, m, rel(a, wa), rel(y, wy))
+            assert np.all(a >= 0)
+            ctx.set_factor(m, wa, wy)
+            pos += 2 * n
+    np.testing.assert_array_equal(np.array(accs, np.uint64), golden[f"t1_snmc_{tag}_acc"])
+    print(f"max rel err {tag}: {worst:.3e}")
+
+
+def test_s_nmc_4way(ntc, golden):
+    dims = [int(d) for d in golden["t4_dims"]]
+    ctx = ctx_for(ntc, dims, golden["t4_idx"], golden["t4_vals"])
+    ctx.set_factors(3, _split(golden["t4_init"], dims, 3))
+    cfg = ntc.NmcConfig(lambda_=1e-2, c=0.6, max_inner=2)
+    want = golden["t4_snmc"]
+    pos = 0
+    for k in range(2):
+        for m in range(4):
+            ctx.s_nmc(m, cfg, O.Oracle().sweep_state(5, k, m))
+            a, _ = ctx.get_factor(m)
+            w = want[pos: pos + dims[m] * 3].reshape(dims[m], 3)
+            assert rel(a, w) <= TOL
+            ctx.set_factor(m, w)
+            pos += dims[m] * 3
+
+
+def test_s_nmc_reference_api(ntc, golden, orc):
+    """ntc.s_nmc(tensor, factors, mode, a_init, cfg, rng, stats) like nmc.hpp:93-95."""
+    dims = [int(d) for d in golden["t1_dims"]]
+    t = ntc.SparseTensor(dims, golden["t1_idx"], golden["t1_vals"])
+    f = ntc.FactorSet(5, _split(golden["t1_init"], dims, 5), _split(golden["t1_init"], dims, 5))
+    st = ntc.SnmcStats()
+    cfg = ntc.NmcConfig(c=0.5, max_inner=2)
+    out = ntc.s_nmc(t, f, 0, f.factors[0], cfg, ntc.sweep_stream(11, 0, 0), st)
+    want = golden["t1_snmc_c05_i2"][: dims[0] * 5].reshape(dims[0], 5)
+    assert rel(out, want) <= TOL
+    assert st.entries_accessed == golden["t1_snmc_c05_i2_acc"][0]
+    ntc.s_nmc(t, f, 0, f.factors[0], cfg, ntc.sweep_stream(11, 0, 0), st)
+    assert st.entries_accessed == 2 * golden["t1_snmc_c05_i2_acc"][0]  # += (nmc.cpp:270)
+    with pytest.raises(ValueError, match="a_init must be nonnegative"):
+        bad = f.factors[0].copy()
+        bad[0, 0] = -0.1
+        ntc.s_nmc(t, f, 0, bad, cfg, ntc.RngStream(6))
+    with pytest.raises(ValueError, match="a_init shape mismatch"):
+        ntc.s_nmc(t, f, 0, np.zeros((2, 2)), cfg, ntc.RngStream(6))
+    with pytest.raises(ValueError, match="mode out of range"):
+        ntc.s_nmc(t, f, 5, f.factors[0], cfg, ntc.RngStream(6))
+    with pytest.raises(ValueError, match="lambda must be > 0"):
+        ntc.s_nmc(t, f, 0, f.factors[0], ntc.NmcConfig(lambda_=0.0), ntc.RngStream(6))
+
+
+def test_s_nmc_edge_cases(ntc):
+    # max_inner = 0 -> a_init unchanged, nothing accessed (test_nmc.cpp:279-302)
+    rng = np.random.default_rng(3)
+    dims = [4, 3, 3]
+    cells = rng.choice(36, 18, replace=False)
+    idx = np.stack(np.unravel_index(cells, dims), 1).astype(np.uint32)
+    t = ntc.SparseTensor(dims, idx, rng.random(18))
+    f = ntc.FactorSet.random_uniform(dims, 2, ntc.RngStream(2))
+    a0 = f.factors[0].astype(np.float32).astype(np.float64)
+    f.factors[0] = a0.copy()
+    st = ntc.SnmcStats()
+    out = ntc.s_nmc(t, f, 0, a0, ntc.NmcConfig(max_inner=0), ntc.RngStream(1), st)
+    np.testing.assert_array_equal(out, a0)
+    assert st.entries_accessed == 0
+    # empty tensor: every row skipped
+    te = ntc.SparseTensor([4, 3, 3], np.zeros((0, 3), np.uint32), np.zeros(0))
+    fe = ntc.FactorSet.random_uniform([4, 3, 3], 2, ntc.RngStream(2))
+    fe.factors = [u.astype(np.float32).astype(np.float64) for u in fe.factors]
+    init2 = fe.factors[1].copy()
+    st = ntc.SnmcStats()
+    out = ntc.s_nmc(te, fe, 1, init2, ntc.NmcConfig(max_inner=5), ntc.RngStream(3), st)
+    np.testing.assert_array_equal(out, init2)
+    np.testing.assert_array_equal(fe.momentum[1], init2)
+    assert st.entries_accessed == 0
+    # skip rows whose blocksize floors to zero (test_nmc.cpp:304-319)
+    t2 = ntc.SparseTensor([2, 6], np.array([[0, 0], [0, 1], [0, 2], [0, 3], [1, 5]], np.uint32),
+                          np.array([1, 2, 3, 4, 5.0]))
+    f2 = ntc.FactorSet.random_uniform([2, 6], 2, ntc.RngStream(9))
+    f2.factors = [u.astype(np.float32).astype(np.float64) for u in f2.factors]
+    a_init = f2.factors[0].copy()
+    st = ntc.SnmcStats()
+    out = ntc.s_nmc(t2, f2, 0, a_init, ntc.NmcConfig(c=0.3), ntc.RngStream(4), st)
+    assert st.entries_accessed == 1
+    np.testing.assert_array_equal(out[1], a_init[1])
+    np.testing.assert_array_equal(f2.momentum[0][1], a_init[1])
+    assert out[0, 0] != a_init[0, 0]
+
+
+def test_s_nmc_nonfinite_diagnostic(ntc):
+    dims = [3, 4, 2]
+    idx = np.array([[i, j, k] for i in range(3) for j in range(4) for k in range(2)], np.uint32)
+    t = ntc.SparseTensor(dims, idx, np.ones(len(idx)))
+    f = ntc.FactorSet.random_uniform(dims, 2, ntc.RngStream(1))
+    f.factors = [u.astype(np.float32).astype(np.float64) for u in f.factors]
+    f.factors[1][2, :] = 1e200  # k = inf (in fp64 too): non-finite gradient on every row
+    f.factors[2][:, :] = 1e200
+    with pytest.raises(RuntimeError, match=r"s_nmc: non-finite gradient at row 1 \(mode 1\)"):
+        ntc.s_nmc(t, f, 0, f.factors[0], ntc.NmcConfig(), ntc.RngStream(1))
+
+
+def test_c1_seed_independence_and_determinism(ntc):
+    import paper_2109_09534_b200 as P
+    ctx = P.Context(0)
+    ctx.synth_uniform([60, 50, 40], 30000, 4, 0.01, 77)
+    ctx.random_factors(6, 7)
+    a0 = [ctx.get_factor(m)[0] for m in range(3)]
+
+    def run(seed, c):
+        for m in range(3):
+            ctx.set_factor(m, a0[m], a0[m])
+        for k in range(3):
+            ctx.sweep_async(k, P.NmcConfig(c=c, max_inner=2), seed)
+        ctx.collect()
+        return [ctx.get_factor(m)[0] for m in range(3)]
+
+    r1, r2 = run(1, 1.0), run(999, 1.0)
+    for a, b in zip(r1, r2):
+        np.testing.assert_array_equal(a, b)
+    s1, s2, s3 = run(5, 0.5), run(5, 0.5), run(6, 0.5)
+    for a, b in zip(s1, s2):
+        np.testing.assert_array_equal(a, b)  # bitwise deterministic
+    assert any(not np.array_equal(a, b) for a, b in zip(s1, s3))
+    assert all(np.all(a >= 0) for a in s1)
+
+
+# ---------------------------------------------------------------- AO driver + metrics
+def test_metrics_match_reference(ntc, golden):
+    dims = [int(d) for d in golden["t1_dims"]]
+    t = ntc.SparseTensor(dims, golden["t1_idx"], golden["t1_vals"])
+    f = ntc.FactorSet(5, _split(golden["t1_init"], dims, 5), _split(golden["t1_init"], dims, 5))
+    obj, rl = golden["t1_metrics_init"]
+    assert abs(ntc.objective(t, f, 1e-3) - obj) <= 1e-9 * abs(obj)
+    assert abs(ntc.relative_error(t, f) - rl) <= 1e-9 * abs(rl)
+
+
+def test_ao_ntc_matches_reference(ntc, golden):
+    dims = [int(d) for d in golden["t2_dims"]]
+    t = ntc.SparseTensor(dims, golden["t2_idx"], golden["t2_vals"])
+    init = ntc.FactorSet(3, _split(golden["t2_init"], dims, 3), _split(golden["t2_init"], dims, 3))
+    seen = []
+    res = ntc.ao_ntc(t, init, ntc.AoConfig(rank=3, c=0.5, max_epochs=6.0, seed=11),
+                     lambda r, f: seen.append((r.epoch, f.all_nonnegative())))
+    h = golden["t2_ao_hist"]
+    assert len(res.history) == len(h) == len(seen)
+    for r, w in zip(res.history, h):
+        assert r.epoch == w[0] and r.entries_accessed == int(w[4])
+        assert abs(r.objective - w[1]) <= TOL * abs(w[1])
+        assert abs(r.rel_error - w[2]) <= TOL * abs(w[2])
+    want = _split(golden["t2_ao_factors"], dims, 3)
+    for a, b in zip(res.factors.factors, want):
+        assert rel(a, b) <= TOL
+    # metrics_every thins records, final state kept (test_ao.cpp:215-233)
+    res2 = ntc.ao_ntc(t, init, ntc.AoConfig(rank=3, c=1.0, max_epochs=15.0, seed=3, metrics_every=2))
+    assert [r.epoch for r in res2.history] == list(golden["t2_ao_every2_hist"][:, 0])
+    for a, b in zip(res2.factors.factors, _split(golden["t2_ao_every2_factors"], dims, 3)):
+        assert rel(a, b) <= TOL
+
+
+def test_ao_zero_progress_and_budget(ntc):
+    t = ntc.SparseTensor([3, 3, 3], np.array([[0, 0, 0], [1, 1, 1], [2, 2, 2]], np.uint32),
+                         np.array([1.0, 2.0, 3.0]))
+    init = ntc.initial_factors([3, 3, 3], 2, 7)
+    init.factors = [u.astype(np.float32).astype(np.float64) for u in init.factors]
+    res = ntc.ao_ntc(t, init, ntc.AoConfig(rank=2, c=0.5, max_epochs=100.0))
+    assert len(res.history) == 1 and res.history[0].epoch == 0.0
+    np.testing.assert_array_equal(res.factors.factors[0], init.factors[0])
+    res = ntc.ao_ntc(t, init, ntc.AoConfig(rank=2, max_epochs=0.0))
+    assert len(res.history) == 1
+
+
+# ---------------------------------------------------------------- trajectory at scale
+def test_trajectory_20_iterations_vs_oracle(ntc, orc):
+    """Free-running 20 AO iterations on a 1%-dense 160^3 tensor (cfg-1 style,
+    R = 10, c = 0.5): device fp32 vs restated reference fp64, same seeds; the
+    per-iteration relative factor error must stay <= 1e-4."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [160, 160, 160], 40960, 10
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, nnz, 10, 0.01, 1001)
+    ci, cv = ctx.canonical()
+    cv64 = cv.astype(np.float64)
+    views = [orc.build_view(dims, ci, cv64, m) for m in range(3)]
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 7)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    cfg = P.NmcConfig(c=0.5)
+    ocfg = O.nmc_cfg(c=0.5, threads=8)
+    worst = []
+    for k in range(20):
+        ctx.sweep_async(k, cfg, 7)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None, ocfg, orc.sweep_state(7, k, m))
+                   for m in range(3))
+        assert acc == oacc
+        errs = [rel(ctx.get_factor(m)[0], F[m]) for m in range(3)]
+        worst.append(max(errs))
+        assert max(errs) <= TOL, (k, errs)
+    sse, den, _ = orc.metrics(dims, R, F, ci, cv64)
+    assert abs(ctx.relative_error() - np.sqrt(sse / den)) <= 1e-5 * np.sqrt(sse / den)
+    print("per-iteration max rel err:", " ".join(f"{w:.1e}" for w in worst))
+
+
+def test_cfg1_scale_properties(ntc):
+    """BASELINE configs[0] shape at full size: size-independent invariants."""
+    import paper_2109_09534_b200 as P
+    dims, nnz = [500, 500, 500], 1_250_000
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, nnz, 10, 0.01, 1001)
+    order, d, n = ctx.info()
+    assert n == nnz and d == dims
+    expect = 0
+    for m in range(3):
+        off, oth, val = ctx.view(m)
+        assert off[-1] == nnz and np.all(np.diff(off.astype(np.int64)) >= 0)
+        assert np.all(val >= 0)
+        expect += int(sum(np.floor(0.5 * np.diff(off.astype(np.float64)))))
+    ctx.random_factors(10, 7)
+    r0 = ctx.relative_error()
+    for k in range(5):
+        ctx.sweep_async(k, P.NmcConfig(c=0.5), 7)
+    assert ctx.collect() == 5 * expect
+    r1 = ctx.relative_error()
+    assert r1 < r0
+    for m in range(3):
+        assert np.all(ctx.get_factor(m)[0] >= 0)
