@@ -119,6 +119,10 @@ int ntcb_tensor_info(ntcb_context* ctx, int* order, uint64_t* dims, uint64_t* nn
  * others[nnz*(order-1)], values[nnz]; any pointer may be NULL. */
 int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* others,
                      float* values);
+/* Rows [row_begin, row_end) of a view: offsets[row_end-row_begin+1]
+ * (absolute entry positions), others/values of those slices only. */
+int ntcb_view_export_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
+                          uint64_t* offsets, uint32_t* others, float* values);
 /* Canonical (lexicographic) COO, SparseTensor::indices()/values(). */
 int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values);
 

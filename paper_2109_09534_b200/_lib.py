@@ -81,6 +81,8 @@ SIGNATURES = {
                                           C.c_void_p]),
     "ntcb_tensor_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), u64p, u64p]),
     "ntcb_view_export": (C.c_int, [C.c_void_p, C.c_int, u64p, u32p, f32p]),
+    "ntcb_view_export_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, u64p, u32p,
+                                        f32p]),
     "ntcb_tensor_export": (C.c_int, [C.c_void_p, u32p, f32p]),
     "ntcb_factors_init": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(f64p), C.POINTER(f64p)]),
     "ntcb_factors_random": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),

@@ -371,6 +371,28 @@ int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* o
   API_CATCH
 }
 
+int ntcb_view_export_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
+                          uint64_t* offsets, uint32_t* others, float* values) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_export: mode out of range");
+  const DeviceView& v = ctx->views[mode];
+  if (row_begin > row_end || row_end > v.rows) fail(NTCB_ERANGE, "view_export: rows out of range");
+  const uint64_t e0 = v.h_off[row_begin], e1 = v.h_off[row_end], n = e1 - e0;
+  const int no = ctx->order - 1;
+  if (offsets) std::memcpy(offsets, v.h_off + row_begin, sizeof(uint64_t) * (row_end - row_begin + 1));
+  if (others && n) {
+    std::vector<uint32_t> col(n);
+    for (int k = 0; k < no; ++k) {
+      NTCB_CUDA(cudaMemcpy(col.data(), v.oth[k] + e0, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+      for (uint64_t t = 0; t < n; ++t) others[t * no + k] = col[t];
+    }
+  }
+  if (values && n) NTCB_CUDA(cudaMemcpy(values, v.val + e0, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  API_CATCH
+}
+
 int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values) {
   API_TRY
   need_ctx(ctx);

@@ -1,0 +1,112 @@
+"""Multi-GPU S_NMC: one process per GPU, rows of the factor being updated
+sharded across ranks, an all-gather of the updated factor after every mode
+update.
+
+* Rows are independent within a mode update and every row's stream is keyed
+  by (sweep, mode, inner iteration, row) -- never by rank (nmc.cpp:231-236) --
+  so results are bit-identical for any number of GPUs.
+* Each rank updates a contiguous row range chosen by prefix sums of work
+  (sampled entries + a per-row overhead), not equal row counts, and holds
+  replicas of every factor; only A^(n) is exchanged (I_n x ld fp32), Y stays
+  local (it is reset at every S_NMC call, nmc.cpp:212-215).
+* The exchange is a torch.distributed all-gather (NCCL over NVLink on GPUs,
+  gloo in the CPU tests) of padded shards into the resident factor memory.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+ROW_OVERHEAD = 64  # entry-equivalents of fixed per-row cost (finalise + power method)
+
+
+def blocksizes(offsets: np.ndarray, c: float) -> np.ndarray:
+    """floor(c * n_p) per row in double, n_p at c >= 1 (nmc.cpp:36-40)."""
+    n = np.diff(np.asarray(offsets, np.uint64)).astype(np.float64)
+    if c >= 1.0:
+        return n.astype(np.uint64)
+    return np.minimum(np.floor(c * n), n).astype(np.uint64)
+
+
+def partition_rows(offsets: np.ndarray, c: float, world: int) -> List[Tuple[int, int]]:
+    """Contiguous row ranges, one per rank, balancing sum(b_p + ROW_OVERHEAD).
+    Streaming cost is ~n_p, sampling/accumulation ~b_p; both are known before
+    the run because b_p does not depend on the RNG."""
+    n = np.diff(np.asarray(offsets, np.uint64)).astype(np.float64)
+    b = blocksizes(offsets, c).astype(np.float64)
+    work = np.where(b > 0, 0.5 * n + b + ROW_OVERHEAD, 1.0)
+    cum = np.concatenate([[0.0], np.cumsum(work)])
+    total = cum[-1]
+    rows = len(n)
+    cuts = [0]
+    for k in range(1, world):
+        cuts.append(int(np.searchsorted(cum, total * k / world, side="left")))
+    cuts.append(rows)
+    cuts = [min(max(x, 0), rows) for x in cuts]
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+def allgather_rows(t, bounds: Sequence[Tuple[int, int]], rank: int, group=None) -> None:
+    """In place: every rank's rows bounds[k] of the 2-D tensor t (rows x ld)
+    are replaced by rank k's copy.  One padded all-gather."""
+    import torch
+    import torch.distributed as dist
+    world = len(bounds)
+    S = max(1, max(r1 - r0 for r0, r1 in bounds))
+    r0, r1 = bounds[rank]
+    send = torch.zeros((S, t.shape[1]), dtype=t.dtype, device=t.device)
+    if r1 > r0:
+        send[: r1 - r0].copy_(t[r0:r1])
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    for k, (a, b) in enumerate(bounds):
+        if k != rank and b > a:
+            t[a:b].copy_(recv[k][: b - a])
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer owned by libntcb."""
+
+    def __init__(self, ptr: int, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def factor_tensor(ctx, mode: int, rows: int, which: int = 0):
+    """torch view (rows x ld, fp32, cuda) of the resident factor (A or Y)."""
+    import torch
+    ptr, ld = ctx.factor_device_ptr(mode, which)
+    return torch.as_tensor(_CudaArray(ptr, (rows, ld)), device=f"cuda:{ctx.device}")
+
+
+class ShardedSweep:
+    """Drives ntcb over this rank's row shard of every mode, then all-gathers."""
+
+    def __init__(self, ctx, cfg, rank: int, world: int, group=None):
+        import torch
+        self.ctx, self.cfg, self.rank, self.world, self.group = ctx, cfg, rank, world, group
+        order, dims, _ = ctx.info()
+        self.dims = dims
+        self.bounds = [partition_rows(ctx.view_offsets(m), cfg.c, world) for m in range(order)]
+        self.A = [factor_tensor(ctx, m, dims[m]) for m in range(order)]
+        st = torch.cuda.current_stream()
+        if st.cuda_stream == 0:  # legacy default stream has no handle; use a real one
+            st = torch.cuda.Stream()
+            torch.cuda.set_stream(st)
+        ctx.set_stream(st.cuda_stream)
+
+    def sweep(self, k: int, seed: int) -> None:
+        from .ntc import sweep_stream
+        for m in range(len(self.dims)):
+            r0, r1 = self.bounds[m][self.rank]
+            self.ctx.s_nmc_rows_async(m, r0, r1, self.cfg, sweep_stream(seed, k, m).state)
+            if self.world > 1:
+                allgather_rows(self.A[m], self.bounds[m], self.rank, self.group)
+
+    def local_sampled(self, m: int) -> int:
+        r0, r1 = self.bounds[m][self.rank]
+        off = self.ctx.view_offsets(m)
+        return int(blocksizes(off[r0: r1 + 1], self.cfg.c).sum()) * self.cfg.max_inner

@@ -236,6 +236,28 @@ class Context:
                                       oth.ctypes.data_as(u32p), val.ctypes.data_as(f32p)))
         return off, oth[: nnz * (order - 1)].reshape(nnz, order - 1), val[:nnz]
 
+    def view_offsets(self, mode):
+        order, dims, nnz = self.info()
+        off = np.zeros(dims[mode] + 1, np.uint64)
+        check(self.L.ntcb_view_export(self.h, mode, off.ctypes.data_as(u64p), None, None))
+        return off
+
+    def view_rows(self, mode, row_begin, row_end):
+        """(offsets rebased to 0, others, values) of the slices of rows [row_begin, row_end)."""
+        order, dims, nnz = self.info()
+        off = np.zeros(row_end - row_begin + 1, np.uint64)
+        check(self.L.ntcb_view_export_rows(self.h, mode, row_begin, row_end,
+                                           off.ctypes.data_as(u64p), None, None))
+        n = int(off[-1] - off[0])
+        oth = np.zeros(max(n * (order - 1), 1), np.uint32)
+        val = np.zeros(max(n, 1), np.float32)
+        check(self.L.ntcb_view_export_rows(self.h, mode, row_begin, row_end, None,
+                                           oth.ctypes.data_as(u32p), val.ctypes.data_as(f32p)))
+        return off - off[0], oth[: n * (order - 1)].reshape(n, order - 1), val[:n]
+
+    def set_stream(self, stream_ptr):
+        check(self.L.ntcb_set_stream(self.h, C.c_void_p(stream_ptr)))
+
     def canonical(self):
         order, dims, nnz = self.info()
         idx = np.zeros(max(nnz * order, 1), np.uint32)
@@ -286,6 +308,15 @@ class Context:
             ai = np.ascontiguousarray(a_init, np.float64)
         check(self.L.ntcb_s_nmc(self.h, mode, None if ai is None else ai.ctypes.data_as(f64p),
                                 C.byref(cs), rng_state, C.byref(acc)))
+        return acc.value
+
+    def s_nmc_host(self, mode, a_init, a_out, y_out, cfg: NmcConfig, rng_state: int) -> int:
+        """Host-buffer drop-in (ntcb_s_nmc_host): float64 (rows, R) arrays in/out."""
+        acc = C.c_uint64(0)
+        cs = cfg.c_struct()
+        check(self.L.ntcb_s_nmc_host(self.h, mode, a_init.ctypes.data_as(f64p),
+                                     a_out.ctypes.data_as(f64p), y_out.ctypes.data_as(f64p),
+                                     C.byref(cs), rng_state, C.byref(acc)))
         return acc.value
 
     def s_nmc_rows_async(self, mode, row_begin, row_end, cfg: NmcConfig, rng_state: int):
