@@ -14,10 +14,11 @@
 #include "common.cuh"
 
 namespace ntcb {
-int launch_sample(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end, double c,
-                  uint64_t root, uint32_t* dbg_picks, const uint64_t* dbg_off, int direct = 0);
+int launch_sample(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
+                  uint64_t row_begin, uint64_t row_end, double c, uint64_t root,
+                  uint32_t* dbg_picks, const uint64_t* dbg_off, int direct = 0);
 int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
-                  const ntcb_nmc_config& cfg);
+                  const ntcb_nmc_config& cfg, const uint32_t* mask);
 void free_views(ntcb_context* ctx);
 void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                      const uint32_t* h_idx, const double* h_vals);
@@ -93,22 +94,24 @@ uint64_t blocksize_sum(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, do
   return s;
 }
 
-void prof_mark(ntcb_context* ctx, int kind) {
+void prof_mark(ntcb_context* ctx, int kind, cudaStream_t st) {
   Profile& pf = ctx->prof;
   if (!pf.on) return;
   if (pf.n + 2 > 4096) return;
-  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], ctx->stream));
+  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], st));
   pf.kind[pf.n / 2] = kind;
   pf.n += 1;
 }
-void prof_end(ntcb_context* ctx) {
+void prof_end(ntcb_context* ctx, cudaStream_t st) {
   Profile& pf = ctx->prof;
   if (!pf.on || (pf.n & 1) == 0) return;
-  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], ctx->stream));
+  NTCB_CUDA(cudaEventRecord(pf.ev[pf.n], st));
   pf.n += 1;
 }
 
 // Queue one s_nmc on rows [r0, r1) of `mode` with a_init == factors[mode].
+// Sampling runs on the side stream (it never reads factors), so the sample of
+// the next mode overlaps this mode's update; events order mask reuse.
 void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
                   const ntcb_nmc_config& cfg, uint64_t rng_state) {
   const uint64_t ld = ctx->ld;
@@ -121,18 +124,27 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
   for (int l = 0; l < cfg.max_inner; ++l) {
     const uint64_t root = fork64(rng_state, static_cast<uint64_t>(l));
+    const int par = ctx->mask_parity[mode];
+    ctx->mask_parity[mode] ^= 1;
+    uint32_t* mask = ctx->mask[mode][par];
     if (cfg.c < 1.0 && e1 > e0) {
+      if (ctx->consumed_valid[mode][par])
+        NTCB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_consumed[mode][par], 0));
       const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
-      NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), st));
-      prof_mark(ctx, 1);
-      ctx->prof.launches += launch_sample(ctx, mode, r0, r1, cfg.c, root, nullptr, nullptr);
-      prof_end(ctx);
+      NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->side));
+      prof_mark(ctx, 1, ctx->side);
+      ctx->prof.launches += launch_sample(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, nullptr, nullptr);
+      prof_end(ctx, ctx->side);
+      NTCB_CUDA(cudaEventRecord(ctx->ev_sampled[mode][par], ctx->side));
+      NTCB_CUDA(cudaStreamWaitEvent(st, ctx->ev_sampled[mode][par], 0));
     }
-    prof_mark(ctx, 0);
-    const int n = launch_update(ctx, mode, r0, r1, cfg);
+    prof_mark(ctx, 0, st);
+    const int n = launch_update(ctx, mode, r0, r1, cfg, mask);
     ctx->prof.launches += n;
     ctx->prof.update_launches += n;
-    prof_end(ctx);
+    prof_end(ctx, st);
+    NTCB_CUDA(cudaEventRecord(ctx->ev_consumed[mode][par], st));
+    ctx->consumed_valid[mode][par] = true;
   }
   g_host[ctx].pending_accessed +=
       static_cast<uint64_t>(cfg.max_inner) * blocksize_sum(ctx, mode, r0, r1, cfg.c);
@@ -140,6 +152,7 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
 
 // Waits and converts a device-side row failure into the reference's exception.
 void collect(ntcb_context* ctx, uint64_t* accessed) {
+  NTCB_CUDA(cudaStreamSynchronize(ctx->side));
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   NTCB_CUDA(cudaMemcpy(ctx->h_counters, ctx->counters, 2 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost));
@@ -253,9 +266,14 @@ int ntcb_create(int device, ntcb_context** out) {
   NTCB_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   ctx->stream = ctx->own_stream;
   NTCB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
-  NTCB_CUDA(cudaMalloc(&ctx->counters, 2 * sizeof(unsigned long long)));
-  NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 2 * sizeof(unsigned long long)));
-  const unsigned long long init[2] = {0, ~0ull};
+  NTCB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  for (auto& mm : ctx->ev_sampled)
+    for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& mm : ctx->ev_consumed)
+    for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NTCB_CUDA(cudaMalloc(&ctx->counters, 4 * sizeof(unsigned long long)));
+  NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 4 * sizeof(unsigned long long)));
+  const unsigned long long init[4] = {0, ~0ull, 0, 0};
   NTCB_CUDA(cudaMemcpy(ctx->counters, init, sizeof init, cudaMemcpyHostToDevice));
   for (auto& e : ctx->prof.ev) NTCB_CUDA(cudaEventCreate(&e));
   g_host[ctx] = HostState{};
@@ -274,6 +292,11 @@ int ntcb_destroy(ntcb_context* ctx) {
   cudaFree(ctx->counters);
   cudaFreeHost(ctx->h_counters);
   for (auto& e : ctx->prof.ev) cudaEventDestroy(e);
+  for (auto& mm : ctx->ev_sampled)
+    for (auto& e : mm) cudaEventDestroy(e);
+  for (auto& mm : ctx->ev_consumed)
+    for (auto& e : mm) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
   g_host.erase(ctx);
   delete ctx;
@@ -553,12 +576,14 @@ int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
   NTCB_CUDA(cudaMalloc(&d_po, sizeof(uint64_t) * (rows + 1)));
   NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * po[rows]));
   NTCB_CUDA(cudaMemcpy(d_po, po.data(), sizeof(uint64_t) * (rows + 1), cudaMemcpyHostToDevice));
+  collect(ctx, nullptr);
+  uint32_t* mask = ctx->mask[mode][0];
   const uint64_t e0 = off[row_begin], e1 = off[row_end];
   if (e1 > e0) {
     const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
-    NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
+    NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
   }
-  launch_sample(ctx, mode, row_begin, row_end, c, fork64(rng_state, l), d_pk, d_po);
+  launch_sample(ctx, ctx->stream, mask, mode, row_begin, row_end, c, fork64(rng_state, l), d_pk, d_po);
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   NTCB_CUDA(cudaMemcpy(picks, d_pk, sizeof(uint32_t) * po[rows], cudaMemcpyDeviceToHost));
   cudaFree(d_po);
@@ -584,10 +609,12 @@ int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_
   NTCB_CUDA(cudaMalloc(&d_po, sizeof po));
   NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * b));
   NTCB_CUDA(cudaMemcpy(d_po, po, sizeof po, cudaMemcpyHostToDevice));
+  collect(ctx, nullptr);
+  uint32_t* mask = ctx->mask[mode][0];
   const uint64_t e0 = off[row], e1 = off[row + 1];
   const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
-  NTCB_CUDA(cudaMemsetAsync(ctx->mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
-  launch_sample(ctx, mode, row, row + 1, c, row_state, d_pk, d_po, 1);
+  NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
+  launch_sample(ctx, ctx->stream, mask, mode, row, row + 1, c, row_state, d_pk, d_po, 1);
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   NTCB_CUDA(cudaMemcpy(picks, d_pk, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost));
   cudaFree(d_po);
@@ -731,6 +758,7 @@ int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms, u
                       uint64_t* update_launches) {
   API_TRY
   need_ctx(ctx);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->side));
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   Profile& pf = ctx->prof;
   double u = 0.0, s = 0.0;

@@ -108,12 +108,19 @@ struct ntcb_context {
   float* A[NTCB_MAX_ORDER] = {};
   float* Y[NTCB_MAX_ORDER] = {};
 
-  // scratch
-  uint32_t* mask = nullptr;  // one bit per view entry (sampled set)
+  // sampled-set masks, one bit per view entry, per (mode, inner-iteration parity)
+  uint32_t* mask[NTCB_MAX_ORDER][2] = {};
   uint64_t mask_words = 0;
+  int mask_parity[NTCB_MAX_ORDER] = {};
+  cudaStream_t side = nullptr;  // sampler stream (sampling never reads factors)
+  cudaEvent_t ev_sampled[NTCB_MAX_ORDER][2] = {};
+  cudaEvent_t ev_consumed[NTCB_MAX_ORDER][2] = {};
+  bool consumed_valid[NTCB_MAX_ORDER][2] = {};
+  float* partial = nullptr;  // split-row partial sums
+  uint64_t partial_n = 0;
   uint32_t* perm_scratch = nullptr;  // per-entry Fisher-Yates scratch for slices too big for smem
   uint64_t perm_scratch_n = 0;
-  unsigned long long* counters = nullptr;  // [0] entries accessed, [1] first error key
+  unsigned long long* counters = nullptr;  // [1] first error key, [2] work cursor
   unsigned long long* h_counters = nullptr;  // pinned mirror
   double* red = nullptr;  // metrics partials
   uint64_t red_n = 0;

@@ -170,7 +170,10 @@ void radix_pairs(ntcb_context* ctx, KT* keys, KT* keys_alt, uint32_t* vals, uint
 
 }  // namespace
 
+void drop_plans(ntcb_context* ctx);
+
 void free_views(ntcb_context* ctx) {
+  drop_plans(ctx);
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
     DeviceView& v = ctx->views[m];
     if (v.off) cudaFree(v.off);
@@ -180,9 +183,15 @@ void free_views(ntcb_context* ctx) {
     delete[] v.h_off;
     v = DeviceView{};
   }
-  if (ctx->mask) cudaFree(ctx->mask);
-  ctx->mask = nullptr;
+  for (auto& mm : ctx->mask)
+    for (auto& b : mm) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
   ctx->mask_words = 0;
+  if (ctx->partial) cudaFree(ctx->partial);
+  ctx->partial = nullptr;
+  ctx->partial_n = 0;
   if (ctx->perm_scratch) cudaFree(ctx->perm_scratch);
   ctx->perm_scratch = nullptr;
   ctx->perm_scratch_n = 0;
@@ -265,8 +274,8 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
     DeviceView& v = ctx->views[m];
     v.rows = dims[m];
     NTCB_CUDA(cudaMalloc(&v.off, sizeof(uint64_t) * (v.rows + 1)));
-    for (int k = 0; k < order - 1; ++k) NTCB_CUDA(cudaMalloc(&v.oth[k], sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)));
-    NTCB_CUDA(cudaMalloc(&v.val, sizeof(float) * std::max<uint64_t>(nnz, 1)));
+    for (int k = 0; k < order - 1; ++k) NTCB_CUDA(cudaMalloc(&v.oth[k], sizeof(uint32_t) * (nnz + 4)));
+    NTCB_CUDA(cudaMalloc(&v.val, sizeof(float) * (nnz + 4)));
     if (nnz) {
       NTCB_CUDA(cudaMemcpyAsync(mperm.p, perm.p, sizeof(uint32_t) * nnz, cudaMemcpyDeviceToDevice, st));
       k_mode_keys<<<grid_for(nnz, sms), 256, 0, st>>>(d_idx, mperm.p, nnz, order, m, mkey);
@@ -291,8 +300,12 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
     v.max_slice = mx;
   }
   ctx->mask_words = nnz / 32 + 2;
-  NTCB_CUDA(cudaMalloc(&ctx->mask, sizeof(uint32_t) * ctx->mask_words));
-  NTCB_CUDA(cudaMemsetAsync(ctx->mask, 0, sizeof(uint32_t) * ctx->mask_words, st));
+  for (int m = 0; m < order; ++m)
+    for (int q = 0; q < 2; ++q) {
+      NTCB_CUDA(cudaMalloc(&ctx->mask[m][q], sizeof(uint32_t) * ctx->mask_words));
+      NTCB_CUDA(cudaMemsetAsync(ctx->mask[m][q], 0, sizeof(uint32_t) * ctx->mask_words, st));
+      ctx->consumed_valid[m][q] = false;
+    }
   // Per-entry Fisher-Yates scratch for slices beyond the sampler's smem budget.
   uint64_t big = 0;
   for (int m = 0; m < order; ++m) big = std::max(big, ctx->views[m].max_slice);

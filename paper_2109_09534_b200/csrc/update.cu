@@ -1,41 +1,74 @@
-// Row update of S_NMC (nmc.cpp:199-272 minus sampling): for every processed
-// row p of view `mode`, one CTA
-//   1. streams the slice's entries (coalesced SoA loads) and keeps the ones
-//      whose bit is set in the sampled-set mask (all of them at c >= 1);
-//   2. for each kept entry builds the augmented Khatri-Rao row
-//      k~ = [k_1..k_R, s], k = Hadamard product of the other factors' rows
-//      (kr_row, factor_set.cpp:42-64), s = y.k - x (residual at Y);
-//   3. accumulates the Gram matrix  sum k~ k~^T  with a register-tiled 4x4
-//      outer-product scheme: its R x R block is the sampled Hessian minus
-//      lambda I and its last column is w + z (nmc.cpp:68-106);
-//   4. finalises on warp 0 in fp64: H = lambda I + sum k k^T, grad =
-//      sum s k + lambda y, finiteness checks, power method from the
-//      normalised all-ones vector (nmc.cpp:140-172), L = 1.01 * rq
-//      (nmc.cpp:253-254), projected step + Nesterov momentum (nmc.cpp:174-197).
-// fp32 accumulation, fp64 finalisation.  Summation is in slice order rather
-// than draw order (same sampled set, bit-exact; sums agree to fp32 rounding).
+// Row update of S_NMC (nmc.cpp:199-272 minus sampling).
+//
+// Work decomposition.  A work item is (row p, entry range [e0, e1)) of one
+// mode view: one item per row when the slice has <= kSeg entries, several
+// when it is longer (their partial sums go to a global slot and
+// k_finalize reduces them in a fixed order -- deterministic, and a heavy row
+// no longer serialises on one warp).  ONE WARP per item, no block barriers:
+//
+//   stream  32 consecutive entries per step (coalesced SoA loads), keep the
+//           sampled ones (mask bit, or all at c >= 1), compact them with a
+//           ballot into a 64-slot staging ring in shared memory;
+//   gather  per 32 staged picks, lane i forms k = Hadamard product of the
+//           other factors' rows of pick i (kr_row, factor_set.cpp:42-64,
+//           float4 loads), s = y.k - x, accumulates g += s k in registers
+//           (= w + z of nmc.cpp:84-93) and writes k to a warp-private tile;
+//   Gram    each lane owns a 4x4 block of the R x R upper triangle and a
+//           pick group; 2 LDS.128 + 16 FFMA per pick (nmc.cpp:95-96).
+//
+// Finalisation per row (warp, fp64): H = lambda I + sum k k^T (mirrored),
+// grad = sum s k + lambda y, finiteness checks (nmc.cpp:247-251, 145-146),
+// power method from the normalised all-ones vector (nmc.cpp:140-172),
+// L = 1.01 rq (nmc.cpp:253-254), projected step + Nesterov momentum
+// (nmc.cpp:174-197).  fp32 accumulation; sums are taken in slice order over
+// the (bit-exact) sampled set.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <vector>
+
 #include "common.cuh"
 
 namespace ntcb {
+
+constexpr int kWarps = 8;         // warps per CTA
+constexpr uint64_t kSeg = 16384;  // max entries per work item
+
+struct WorkItem {
+  uint64_t row;
+  uint64_t e0, e1;  // absolute view positions
+  int64_t slot;     // -1: finalise in place; else partial slot
+};
+
+struct FinItem {
+  uint64_t row;
+  int64_t slot0;
+  int32_t nslots;
+};
 
 struct UpdateArgs {
   const uint64_t* off;
   const uint32_t* oth[NTCB_MAX_ORDER - 1];
   const float* val;
   const uint32_t* mask;
-  FactorArgs f;
-  float* A;  // factors[mode]
-  float* Y;  // momentum[mode]
-  uint64_t row_begin, row_end;
+  const float* U[NTCB_MAX_ORDER - 1];  // other modes' factors, ascending mode order
+  int no;                              // order - 1
+  int mode;
+  int rank;
+  float* A;
+  float* Y;
+  const WorkItem* items;
+  uint64_t n_items;
+  const FinItem* fins;
+  uint64_t n_fins;
+  float* partial;  // [slot][R*R + R]
   double c;
   double lambda;
   double power_tol;
   int power_iters;
-  unsigned long long* counters;
+  unsigned long long* counters;  // [1] first error key, [2] item cursor, [3] fin cursor
 };
-
-constexpr int kThreads = 256;
-constexpr int kTile = 512;  // entries examined per tile (2 per thread)
 
 __device__ __forceinline__ void report(unsigned long long* counters, int mode, uint64_t row,
                                        int kind) {
@@ -45,326 +78,542 @@ __device__ __forceinline__ void report(unsigned long long* counters, int mode, u
   atomicMin(&counters[1], key);
 }
 
-template <int RP>
-__global__ void __launch_bounds__(kThreads, 2) k_update(UpdateArgs a) {
-  constexpr int NB4 = RP / 4;
-  constexpr int NBLK = NB4 * (NB4 + 1) / 2;
-  constexpr int G = (kThreads / NBLK) >= 1 ? (kThreads / NBLK) : 1;
-  extern __shared__ __align__(16) unsigned char smem[];
-  float* K = reinterpret_cast<float*>(smem);                // kTile x RP
-  float* red = K + kTile * RP;                              // G x NBLK x 16 (<= 4096 floats)
-  double* Hd = reinterpret_cast<double*>(red + kThreads * 16);  // R x HS (HS odd stride)
-  const int R = a.f.rank;
-  const int HS = R | 1;
-  double* gd = Hd + R * HS;        // gradient (R)
-  double* vv = gd + 64;            // power-method iterate (R)
-  float* ys = reinterpret_cast<float*>(vv + 64);  // y row, padded to RP
-  int* sidx = reinterpret_cast<int*>(ys + RP);    // kTile selected local indices
-  int* wtot = sidx + kTile;                       // per-warp counts (8) + scratch
+template <int LD4>
+struct Geo {
+  static constexpr int NBLK = LD4 * (LD4 + 1) / 2;
+  static constexpr int GW = NBLK <= 32 ? 32 / NBLK : 1;   // pick groups per warp
+  static constexpr int BPL = NBLK <= 32 ? 1 : (NBLK + 31) / 32;  // blocks per lane
+  static constexpr int KS4 = (LD4 % 2) ? LD4 : LD4 + 1;   // odd float4 stride
+  static constexpr int KS = 4 * KS4;
+};
 
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int wid = tid >> 5;
-  const int ld = a.f.ld;
+// per-warp shared memory (floats unless noted)
+template <int LD4>
+struct WarpSmem {
+  static constexpr int kStage = 256;  // staging ring: < 32 leftover + 128 per batch
+  // layout offsets in 4-byte words
+  static __host__ __device__ constexpr int stage_words(int no) { return (no + 1) * kStage; }
+  // the K tile region is reused for Hf (R x HS) after the pick loop
+  static __host__ __device__ constexpr int ktile_words(int R) {  // Hf (R x HS)
+    return ((R * (R | 1) + 3) / 4) * 4;
+  }
+  static __host__ __device__ constexpr int words(int no, int R) {
+    return stage_words(no) + ktile_words(R) + 64 * 2 * 2;  // + g, v as doubles
+  }
+};
+
+__device__ __forceinline__ void block_of(int blk, int nb4, int& bi, int& bj) {
+  int rem = blk;
+  bi = 0;
+  bj = 0;
+  for (int i = 0; i < nb4; ++i) {
+    const int cnt = nb4 - i;
+    if (rem < cnt) {
+      bi = i;
+      bj = i + rem;
+      return;
+    }
+    rem -= cnt;
+  }
+}
+
+// Warp-level finalisation of one row from Hf (R x HS, fp32 sums of k k^T,
+// full symmetric) and g (fp64 sums of s k, in gd).  Writes A[p], Y[p].
+template <int LD4>
+__device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv,
+                             int lane) {
+  const int R = a.rank;
+  const int HS = R | 1;
+  const int ld = LD4 * 4;
+  const double lam = a.lambda;
+  bool bad = false;
+  for (int r = lane; r < R; r += 32) {
+    gd[r] += lam * static_cast<double>(a.Y[p * ld + r]);
+    bad |= !isfinite(gd[r]);
+  }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 0);  // non-finite gradient
+    return;
+  }
+  bool hbad = false;
+  for (int i = lane; i < R * R; i += 32) hbad |= !isfinite(Hf[(i / R) * HS + (i % R)]);
+  if (__any_sync(0xffffffffu, hbad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 1);  // power_method rejects H
+    return;
+  }
+  const double v0 = 1.0 / sqrt(static_cast<double>(R));
+  for (int r = lane; r < R; r += 32) vv[r] = v0;
+  __syncwarp();
+  double rq = 0.0, rq_prev = 0.0;
+  for (int it = 0; it < a.power_iters; ++it) {
+    double u0 = 0.0, u1 = 0.0;
+    if (lane < R) {
+      const float* hr = Hf + lane * HS;
+      for (int j = 0; j < R; ++j) u0 += (static_cast<double>(hr[j]) + (j == lane ? lam : 0.0)) * vv[j];
+    }
+    if (lane + 32 < R) {
+      const float* hr = Hf + (lane + 32) * HS;
+      for (int j = 0; j < R; ++j)
+        u1 += (static_cast<double>(hr[j]) + (j == lane + 32 ? lam : 0.0)) * vv[j];
+    }
+    double num = 0.0, un2 = u0 * u0 + u1 * u1;
+    if (lane < R) num += vv[lane] * u0;
+    if (lane + 32 < R) num += vv[lane + 32] * u1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      un2 += __shfl_xor_sync(0xffffffffu, un2, o);
+    }
+    rq = num;
+    if (un2 == 0.0) {
+      rq = 0.0;
+      break;
+    }
+    if (it > 0 && fabs(rq - rq_prev) <= a.power_tol * fabs(rq)) break;
+    rq_prev = rq;
+    const double inv = 1.0 / sqrt(un2);
+    __syncwarp();
+    if (lane < R) vv[lane] = u0 * inv;
+    if (lane + 32 < R) vv[lane + 32] = u1 * inv;
+    __syncwarp();
+  }
+  const double L = rq * 1.01;  // nmc.cpp:253-254
+  if (!(L >= lam)) {
+    if (lane == 0) report(a.counters, a.mode, p, 2);  // row_step rejects L
+    return;
+  }
+  const double inv_l = 1.0 / L;
+  const double sl = sqrt(L), sm = sqrt(lam);
+  const double beta = (sl - sm) / (sl + sm);
+  for (int r = lane; r < R; r += 32) {
+    const double y = static_cast<double>(a.Y[p * ld + r]);
+    const double ap = static_cast<double>(a.A[p * ld + r]);
+    const double av = y - inv_l * gd[r];
+    const double an = av > 0.0 ? av : 0.0;
+    a.A[p * ld + r] = static_cast<float>(an);
+    a.Y[p * ld + r] = static_cast<float>(an + beta * (an - ap));
+  }
+}
+
+template <int LD4, int NO>
+__global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(UpdateArgs a) {
+  using W = WarpSmem<LD4>;
+  constexpr int L = LD4;          // feature blocks of 4 = lanes (roles) per pick
+  constexpr int GP = 32 / L;      // picks per group
+  constexpr int ND = L / 2 + 1;   // block pairs per role: (s, s+d), d < ND
+  extern __shared__ __align__(16) float smem_f[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int no = NO < NTCB_MAX_ORDER - 1 ? NO : a.no;  // compile-time for orders 3 and 4
+  const int R = a.rank;
+  const int HS = R | 1;
+  const int ld = LD4 * 4;
+  float* wbase = smem_f + static_cast<size_t>(wid) * W::words(no, R);
+  uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
+  float* st_x = wbase + no * W::kStage;                 // [kStage]
+  float* Hf = wbase + W::stage_words(no);               // [R][HS]
+  double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));  // [64]
+  double* vv = gd + 64;                                             // [64]
   const bool full = a.c >= 1.0;
 
-  // this thread's 4x4 block of the (RP x RP) upper triangle, and its pick group
-  const int grp = tid / NBLK;
-  const int blk = tid - grp * NBLK;
-  const bool acc_on = grp < G;
-  int bi = 0, bj = 0;
-  {
-    int rem = blk;
-    for (int i = 0; i < NB4; ++i) {
-      const int cnt = NB4 - i;
-      if (rem < cnt) {
-        bi = i;
-        bj = i + rem;
-        break;
-      }
-      rem -= cnt;
-    }
-  }
+  // role of this lane: pick slot pk within a group, feature block s
+  const int pk = lane / L;
+  const int s = lane - pk * L;
+  const bool lane_on = pk < GP;
+  int sd[ND];  // partner block of pair d
+#pragma unroll
+  for (int d = 0; d < ND; ++d) sd[d] = (s + d) % L;
+  // with even L the distance-L/2 pairs appear twice: roles s >= L/2 skip them
+  const bool skip_last = (L % 2 == 0) && (s >= L / 2);
 
-  // other modes' factor pointers in ascending mode order (kr_row order)
-  const float* U[NTCB_MAX_ORDER - 1];
-  int no = 0;
-  for (int m = 0; m < a.f.order; ++m)
-    if (m != a.f.mode) U[no++] = a.f.U[m];
-  const int ld4 = ld / 4;
-
-  for (uint64_t p = a.row_begin + blockIdx.x; p < a.row_end; p += gridDim.x) {
+  while (true) {
     if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
-    const uint64_t beg = a.off[p];
-    const uint64_t n = a.off[p + 1] - beg;
-    const uint64_t b = blocksize_for(a.c, n);
-    if (b == 0) continue;  // skipped row: A and Y untouched (nmc.cpp:237)
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(&a.counters[2], 1ull);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const WorkItem w = a.items[it];
+    const uint64_t p = w.row;
 
-    if (tid < RP) ys[tid] = tid < R ? a.Y[p * ld + tid] : 0.f;
-    float acc[16];
+    // y block s (gradient taken at Y, nmc.cpp:244-246)
+    const float4 ys = reinterpret_cast<const float4*>(a.Y + p * ld)[s];
+    float acc[ND][16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = 0.f;
-    __syncthreads();
+    for (int d = 0; d < ND; ++d)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[d][e] = 0.f;
+    float4 gl = make_float4(0.f, 0.f, 0.f, 0.f);
 
-    for (uint64_t t0 = 0; t0 < n; t0 += kTile) {
-      // ---- 1. selection + block compaction ------------------------------
-      bool sel[2];
-      int cnt = 0;
+    int head = 0, cnt = 0;  // staging ring [head, head+cnt)
+
+    // One group of np <= GP picks: lane (pk, s) gathers feature block s of
+    // pick pk from every other factor's row (the L lanes of a pick read one
+    // contiguous row), forms the Khatri-Rao block, the residual s = y.k - x
+    // (segment sum over the pick's L lanes), the gradient block, and the
+    // Gram blocks (s, s+d) with partner blocks fetched by shuffle.
+    auto process_group = [&](int np) {
+      const bool on = lane_on && pk < np;
+      const int sidx = (head + pk) & (W::kStage - 1);
+      float4 kb = make_float4(0.f, 0.f, 0.f, 0.f);
+      float x = 0.f;
+      if (on) {
+        x = st_x[sidx];
+        kb = __ldg(reinterpret_cast<const float4*>(a.U[0] + static_cast<uint64_t>(st_o[sidx]) * ld) + s);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const uint64_t t = t0 + 2 * tid + e;
-        bool s = t < n;
-        if (s && !full) {
-          const uint64_t gb = beg + t;
-          s = (__ldg(&a.mask[gb >> 5]) >> (gb & 31u)) & 1u;
+        for (int m = 1; m < NO; ++m) {
+          if (m < no) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(
+                                       a.U[m] + static_cast<uint64_t>(st_o[m * W::kStage + sidx]) * ld) + s);
+            kb.x *= v.x;
+            kb.y *= v.y;
+            kb.z *= v.z;
+            kb.w *= v.w;
+          }
         }
-        sel[e] = s;
-        cnt += s;
       }
-      int incl = cnt;
+      float dp = ys.x * kb.x;
+      dp = fmaf(ys.y, kb.y, dp);
+      dp = fmaf(ys.z, kb.z, dp);
+      dp = fmaf(ys.w, kb.w, dp);
+      float dot = 0.f;
+      const int base = (lane_on ? pk : 0) * L;
+#pragma unroll
+      for (int t = 0; t < L; ++t) dot += __shfl_sync(0xffffffffu, dp, base + t);
+      const float sres = on ? dot - x : 0.f;
+      gl.x = fmaf(sres, kb.x, gl.x);
+      gl.y = fmaf(sres, kb.y, gl.y);
+      gl.z = fmaf(sres, kb.z, gl.z);
+      gl.w = fmaf(sres, kb.w, gl.w);
+      const float ka[4] = {kb.x, kb.y, kb.z, kb.w};
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        float kp[4];
+        if (d == 0) {
+          kp[0] = kb.x;
+          kp[1] = kb.y;
+          kp[2] = kb.z;
+          kp[3] = kb.w;
+        } else {
+          const int src = base + sd[d];
+          kp[0] = __shfl_sync(0xffffffffu, kb.x, src);
+          kp[1] = __shfl_sync(0xffffffffu, kb.y, src);
+          kp[2] = __shfl_sync(0xffffffffu, kb.z, src);
+          kp[3] = __shfl_sync(0xffffffffu, kb.w, src);
+        }
+        if (d == ND - 1 && skip_last) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c2 = 0; c2 < 4; ++c2) acc[d][4 * r + c2] = fmaf(ka[r], kp[c2], acc[d][4 * r + c2]);
+      }
+      head = (head + np) & (W::kStage - 1);
+      cnt -= np;
+    };
+
+    // ---- stream the item in batches of 128 entries (4 per lane, 128-bit
+    // loads issued independently of the mask), prefetching the next batch
+    // while the current one is compacted and processed ----
+    const uint64_t tb = w.e0 & ~uint64_t(3);  // 16-byte aligned start
+    uint4 nxo[NO], nxv;
+    uint32_t nxm = 0xffffffffu;
+    auto fetch = [&](uint64_t t) {
+      const uint64_t e = t + 4 * lane;
+      if (e < w.e1) {
+#pragma unroll
+        for (int m = 0; m < NO; ++m)
+          if (m < no) nxo[m] = __ldg(reinterpret_cast<const uint4*>(a.oth[m] + e));
+        nxv = __ldg(reinterpret_cast<const uint4*>(a.val + e));
+        if (!full) nxm = __ldg(&a.mask[e >> 5]);
+      }
+    };
+    fetch(tb);
+    for (uint64_t t0 = tb; t0 < w.e1; t0 += 128) {
+      uint4 co[NO];
+#pragma unroll
+      for (int m = 0; m < NO; ++m) co[m] = nxo[m];
+      const uint4 cv = nxv;
+      const uint32_t cm = nxm;
+      if (t0 + 128 < w.e1) fetch(t0 + 128);
+      const uint64_t e = t0 + 4 * lane;
+      uint32_t bits = full ? 0xfu : (cm >> (e & 31u)) & 0xfu;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (e + q < w.e0 || e + q >= w.e1) bits &= ~(1u << q);
+      const int c4 = __popc(bits);
+      int incl = c4;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += v;
       }
-      if (lane == 31) wtot[wid] = incl;
-      __syncthreads();
-      int wbase = 0, nsel = 0;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int slot = head + cnt + incl - c4;
 #pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) {
-        const int v = wtot[w];
-        wbase += (w < wid) ? v : 0;
-        nsel += v;
-      }
-      int slot = wbase + incl - cnt;
+      for (int q = 0; q < 4; ++q) {
+        if ((bits >> q) & 1u) {
+          const int sl = slot & (W::kStage - 1);
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (sel[e]) sidx[slot++] = 2 * tid + e;
-      __syncthreads();
-
-      // ---- 2. gather + augmented Khatri-Rao rows --------------------------
-      for (int s = tid; s < nsel; s += kThreads) {
-        const uint64_t t = beg + t0 + sidx[s];
-        float k[RP];
-        {
-          const float4* r0 = reinterpret_cast<const float4*>(U[0] + static_cast<uint64_t>(__ldg(&a.oth[0][t])) * ld);
-#pragma unroll
-          for (int q = 0; q < RP / 4; ++q) {
-            float4 v = (q < ld4) ? __ldg(r0 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            k[4 * q] = v.x;
-            k[4 * q + 1] = v.y;
-            k[4 * q + 2] = v.z;
-            k[4 * q + 3] = v.w;
-          }
-        }
-        for (int m = 1; m < no; ++m) {
-          const float4* rm = reinterpret_cast<const float4*>(U[m] + static_cast<uint64_t>(__ldg(&a.oth[m][t])) * ld);
-#pragma unroll
-          for (int q = 0; q < RP / 4; ++q) {
-            if (q < ld4) {
-              const float4 v = __ldg(rm + q);
-              k[4 * q] *= v.x;
-              k[4 * q + 1] *= v.y;
-              k[4 * q + 2] *= v.z;
-              k[4 * q + 3] *= v.w;
-            }
-          }
-        }
-        float dot = 0.f;
-#pragma unroll
-        for (int r = 0; r < RP; ++r) dot = fmaf(ys[r], k[r], dot);
-        const float x = __ldg(&a.val[t]);
-#pragma unroll
-        for (int r = 0; r < RP; ++r)
-          if (r >= R) k[r] = (r == R) ? (dot - x) : 0.f;
-        float4* dst = reinterpret_cast<float4*>(K + s * RP);
-#pragma unroll
-        for (int q = 0; q < RP / 4; ++q)
-          dst[q] = make_float4(k[4 * q], k[4 * q + 1], k[4 * q + 2], k[4 * q + 3]);
-      }
-      __syncthreads();
-
-      // ---- 3. register-tiled Gram accumulation ---------------------------
-      if (acc_on) {
-        const float4* K4 = reinterpret_cast<const float4*>(K);
-        for (int s = grp; s < nsel; s += G) {
-          const float4 u = K4[s * NB4 + bi];
-          const float4 w = K4[s * NB4 + bj];
-          const float ua[4] = {u.x, u.y, u.z, u.w};
-          const float wa[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[4 * i + j] = fmaf(ua[i], wa[j], acc[4 * i + j]);
+          for (int m = 0; m < NO; ++m)
+            if (m < no) st_o[m * W::kStage + sl] = q == 0 ? co[m].x : q == 1 ? co[m].y : q == 2 ? co[m].z : co[m].w;
+          st_x[sl] = __uint_as_float(q == 0 ? cv.x : q == 1 ? cv.y : q == 2 ? cv.z : cv.w);
+          ++slot;
         }
       }
-      __syncthreads();
+      cnt += total;
+      __syncwarp();
+      while (cnt >= GP) process_group(GP);
     }
+    if (cnt > 0) process_group(cnt);
 
-    // ---- 4. reduce the pick groups, assemble H (fp64) and grad --------------
-    if (acc_on) {
+    // ---- reduce over the GP pick slots (lanes with equal role s) ----------
 #pragma unroll
-      for (int q = 0; q < 16; ++q) red[(grp * NBLK + blk) * 16 + q] = acc[q];
-    }
-    __syncthreads();
-    const double lam = a.lambda;
-    for (int idx = tid; idx < NBLK * 16; idx += kThreads) {
-      const int bk = idx >> 4, q = idx & 15;
-      float s = 0.f;
-      for (int g = 0; g < G; ++g) s += red[(g * NBLK + bk) * 16 + q];
-      int rem = bk, ci = 0, cj = 0;
-      for (int i = 0; i < NB4; ++i) {
-        const int cn = NB4 - i;
-        if (rem < cn) {
-          ci = i;
-          cj = i + rem;
-          break;
+    for (int t = 1; t < GP; ++t) {
+      const int src = (lane + t * L) & 31;
+#pragma unroll
+      for (int d = 0; d < ND; ++d)
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2) {
+          const float v = __shfl_sync(0xffffffffu, acc[d][e2], src);
+          if (pk == 0) acc[d][e2] += v;
         }
-        rem -= cn;
-      }
-      const int row = 4 * ci + (q >> 2), col = 4 * cj + (q & 3);
-      if (row < R && col < R) {
-        if (row <= col) {
-          const double hv = static_cast<double>(s) + (row == col ? lam : 0.0);
-          Hd[row * HS + col] = hv;
-          Hd[col * HS + row] = hv;
-        }
-      } else if (row < R && col == R) {
-        gd[row] = static_cast<double>(s) + lam * static_cast<double>(ys[row]);
+      const float gx = __shfl_sync(0xffffffffu, gl.x, src);
+      const float gy = __shfl_sync(0xffffffffu, gl.y, src);
+      const float gz = __shfl_sync(0xffffffffu, gl.z, src);
+      const float gw = __shfl_sync(0xffffffffu, gl.w, src);
+      if (pk == 0) {
+        gl.x += gx;
+        gl.y += gy;
+        gl.z += gz;
+        gl.w += gw;
       }
     }
-    __syncthreads();
-
-    // ---- 5. warp 0: checks, power method, projected Nesterov step ---------
-    if (wid == 0) {
-      bool bad = false;
-      for (int r = lane; r < R; r += 32) bad |= !isfinite(gd[r]);
-      if (__any_sync(0xffffffffu, bad)) {
-        if (lane == 0) report(a.counters, a.f.mode, p, 0);  // non-finite gradient
-      } else {
-        bool hbad = false;
-        for (int i = lane; i < R * R; i += 32) hbad |= !isfinite(Hd[(i / R) * HS + (i % R)]);
-        if (__any_sync(0xffffffffu, hbad)) {
-          if (lane == 0) report(a.counters, a.f.mode, p, 1);  // power_method rejects H
-        } else {
-          const double v0 = 1.0 / sqrt(static_cast<double>(R));
-          for (int r = lane; r < R; r += 32) vv[r] = v0;
-          __syncwarp();
-          double rq = 0.0, rq_prev = 0.0;
-          for (int it = 0; it < a.power_iters; ++it) {
-            double u0 = 0.0, u1 = 0.0;
-            if (lane < R) {
-              const double* hr = Hd + lane * HS;
-              for (int j = 0; j < R; ++j) u0 += hr[j] * vv[j];
-            }
-            if (lane + 32 < R) {
-              const double* hr = Hd + (lane + 32) * HS;
-              for (int j = 0; j < R; ++j) u1 += hr[j] * vv[j];
-            }
-            double num = 0.0, un2 = u0 * u0 + u1 * u1;
-            if (lane < R) num += vv[lane] * u0;
-            if (lane + 32 < R) num += vv[lane + 32] * u1;
+    __syncwarp();
+    if (pk == 0) {  // lanes 0..L-1: role s holds blocks (s, s+d) and gradient block s
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-              num += __shfl_xor_sync(0xffffffffu, num, o);
-              un2 += __shfl_xor_sync(0xffffffffu, un2, o);
-            }
-            rq = num;
-            if (un2 == 0.0) {
-              rq = 0.0;
-              break;
-            }
-            if (it > 0 && fabs(rq - rq_prev) <= a.power_tol * fabs(rq)) break;
-            rq_prev = rq;
-            const double inv = 1.0 / sqrt(un2);
-            __syncwarp();
-            if (lane < R) vv[lane] = u0 * inv;
-            if (lane + 32 < R) vv[lane + 32] = u1 * inv;
-            __syncwarp();
-          }
-          const double L = rq * 1.01;  // nmc.cpp:253-254
-          if (!(L >= lam)) {
-            if (lane == 0) report(a.counters, a.f.mode, p, 2);  // row_step rejects L
-          } else {
-            const double inv_l = 1.0 / L;
-            const double sl = sqrt(L), sm = sqrt(lam);
-            const double beta = (sl - sm) / (sl + sm);
-            for (int r = lane; r < R; r += 32) {
-              const double y = static_cast<double>(ys[r]);
-              const double ap = static_cast<double>(a.A[p * ld + r]);
-              const double av = y - inv_l * gd[r];
-              const double an = av > 0.0 ? av : 0.0;
-              a.A[p * ld + r] = static_cast<float>(an);
-              a.Y[p * ld + r] = static_cast<float>(an + beta * (an - ap));
-            }
+      for (int d = 0; d < ND; ++d) {
+        if (d == ND - 1 && skip_last) continue;
+        const int cb = sd[d];
+#pragma unroll
+        for (int e2 = 0; e2 < 16; ++e2) {
+          const int row = 4 * s + (e2 >> 2), col = 4 * cb + (e2 & 3);
+          if (row < R && col < R) {
+            Hf[row * HS + col] = acc[d][e2];
+            Hf[col * HS + row] = acc[d][e2];
           }
         }
       }
+      const float ga[4] = {gl.x, gl.y, gl.z, gl.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * s + q < R) gd[4 * s + q] = static_cast<double>(ga[q]);
     }
-    __syncthreads();
+    __syncwarp();
+    if (w.slot < 0) {
+      finalize_row<LD4>(a, p, Hf, gd, vv, lane);
+    } else {
+      float* dst = a.partial + static_cast<uint64_t>(w.slot) * (R * R + R);
+      for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
+      for (int r = lane; r < R; r += 32) dst[R * R + r] = static_cast<float>(gd[r]);
+    }
+    __syncwarp();
   }
 }
 
-template <int RP>
-static size_t update_smem(int R) {
+// Rows split across several items: sum their partial slots in slot order
+// (deterministic), then the same finalisation.
+template <int LD4>
+__global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
+  using W = WarpSmem<LD4>;
+  extern __shared__ __align__(16) float smem_f[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int R = a.rank;
   const int HS = R | 1;
-  return static_cast<size_t>(kTile) * RP * 4 + kThreads * 16 * 4 +
-         static_cast<size_t>(R) * HS * 8 + 64 * 8 * 2 + RP * 4 + kTile * 4 + 64 * 4;
+  float* wbase = smem_f + static_cast<size_t>(wid) * W::words(a.no, R);
+  float* Hf = wbase + W::stage_words(a.no);
+  double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));
+  double* vv = gd + 64;
+  for (uint64_t f = blockIdx.x * kWarps + wid; f < a.n_fins; f += static_cast<uint64_t>(gridDim.x) * kWarps) {
+    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+    const FinItem fi = a.fins[f];
+    for (int i = lane; i < R * R; i += 32) {
+      float s = 0.f;
+      for (int q = 0; q < fi.nslots; ++q) s += a.partial[static_cast<uint64_t>(fi.slot0 + q) * (R * R + R) + i];
+      Hf[(i / R) * HS + (i % R)] = s;
+    }
+    for (int r = lane; r < R; r += 32) {
+      double s = 0.0;
+      for (int q = 0; q < fi.nslots; ++q)
+        s += static_cast<double>(a.partial[static_cast<uint64_t>(fi.slot0 + q) * (R * R + R) + R * R + r]);
+      gd[r] = s;
+    }
+    __syncwarp();
+    finalize_row<LD4>(a, fi.row, Hf, gd, vv, lane);
+    __syncwarp();
+  }
 }
 
-template <int RP>
-static void launch_rp(ntcb_context* ctx, const UpdateArgs& a, uint64_t rows) {
-  const size_t smem = update_smem<RP>(a.f.rank);
-  NTCB_CUDA(cudaFuncSetAttribute(k_update<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+// ---------------------------------------------------------------------------
+// Host side: work lists (cached per mode/row range/c) and launches.
+// ---------------------------------------------------------------------------
+struct WorkPlan {
+  WorkItem* d_items = nullptr;
+  FinItem* d_fins = nullptr;
+  uint64_t n_items = 0, n_fins = 0, n_slots = 0;
+};
+static std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan> g_plans;
+
+static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, double c) {
+  uint64_t cbits;
+  std::memcpy(&cbits, &c, 8);
+  auto key = std::make_tuple(static_cast<const void*>(ctx->views[mode].off), mode, r0, r1, cbits);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) return it->second;
+  const uint64_t* off = ctx->views[mode].h_off;
+  std::vector<WorkItem> items;
+  std::vector<FinItem> fins;
+  int64_t slot = 0;
+  for (uint64_t p = r0; p < r1; ++p) {
+    const uint64_t n = off[p + 1] - off[p];
+    if (blocksize_for(c, n) == 0) continue;  // skipped row (nmc.cpp:237)
+    if (n <= kSeg) {
+      items.push_back({p, off[p], off[p + 1], -1});
+    } else {
+      const uint64_t ns = (n + kSeg - 1) / kSeg;
+      fins.push_back({p, slot, static_cast<int32_t>(ns)});
+      for (uint64_t s = 0; s < ns; ++s)
+        items.push_back({p, off[p] + s * kSeg, std::min(off[p + 1], off[p] + (s + 1) * kSeg), slot++});
+    }
+  }
+  // longest items first: better tail balance for the dynamic scheduler
+  std::stable_sort(items.begin(), items.end(), [](const WorkItem& x, const WorkItem& y) {
+    return (x.e1 - x.e0) > (y.e1 - y.e0);
+  });
+  WorkPlan pl;
+  pl.n_items = items.size();
+  pl.n_fins = fins.size();
+  pl.n_slots = static_cast<uint64_t>(slot);
+  if (pl.n_items) {
+    NTCB_CUDA(cudaMalloc(&pl.d_items, sizeof(WorkItem) * pl.n_items));
+    NTCB_CUDA(cudaMemcpy(pl.d_items, items.data(), sizeof(WorkItem) * pl.n_items, cudaMemcpyHostToDevice));
+  }
+  if (pl.n_fins) {
+    NTCB_CUDA(cudaMalloc(&pl.d_fins, sizeof(FinItem) * pl.n_fins));
+    NTCB_CUDA(cudaMemcpy(pl.d_fins, fins.data(), sizeof(FinItem) * pl.n_fins, cudaMemcpyHostToDevice));
+  }
+  return g_plans.emplace(key, pl).first->second;
+}
+
+void drop_plans(ntcb_context* ctx) {
+  for (auto it = g_plans.begin(); it != g_plans.end();) {
+    bool mine = false;
+    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
+      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
+    if (mine) {
+      if (it->second.d_items) cudaFree(it->second.d_items);
+      if (it->second.d_fins) cudaFree(it->second.d_fins);
+      it = g_plans.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+template <int LD4, int NO>
+static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
+  NTCB_CUDA(cudaFuncSetAttribute(k_update<LD4, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<RP>, kThreads, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<LD4, NO>, kWarps * 32, smem));
   if (per_sm < 1) per_sm = 1;
-  uint64_t grid = rows;
-  const uint64_t cap = static_cast<uint64_t>(per_sm) * ctx->sm_count;
-  if (grid > cap) grid = cap;
-  k_update<RP><<<static_cast<unsigned>(grid), kThreads, smem, ctx->stream>>>(a);
+  uint64_t grid = (pl.n_items + kWarps - 1) / kWarps;
+  grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+  grid = std::max<uint64_t>(grid, 1);
+  k_update<LD4, NO><<<static_cast<unsigned>(grid), kWarps * 32, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
+  return 1;
+}
+
+template <int LD4>
+static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
+  using W = WarpSmem<LD4>;
+  const size_t smem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 * kWarps;
+  int launches = 0;
+  if (pl.n_items) {
+    if (a.no == 2)
+      launches += launch_items<LD4, 2>(ctx, a, pl, smem);
+    else if (a.no == 3)
+      launches += launch_items<LD4, 3>(ctx, a, pl, smem);
+    else
+      launches += launch_items<LD4, NTCB_MAX_ORDER - 1>(ctx, a, pl, smem);
+  }
+  if (pl.n_fins) {
+    NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    const uint64_t fg = std::min<uint64_t>((pl.n_fins + kWarps - 1) / kWarps,
+                                           static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_finalize<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(a);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
 }
 
 int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
-                  const ntcb_nmc_config& cfg) {
+                  const ntcb_nmc_config& cfg, const uint32_t* mask) {
   if (row_end <= row_begin) return 0;
   const DeviceView& v = ctx->views[mode];
+  const WorkPlan& pl = plan_for(ctx, mode, row_begin, row_end, cfg.c);
+  if (pl.n_items == 0) return 0;
+  const uint64_t R = ctx->rank;
+  if (pl.n_slots) {
+    const uint64_t need = pl.n_slots * (R * R + R);
+    if (ctx->partial_n < need) {
+      if (ctx->partial) cudaFree(ctx->partial);
+      NTCB_CUDA(cudaMalloc(&ctx->partial, sizeof(float) * need));
+      ctx->partial_n = need;
+    }
+  }
   UpdateArgs a{};
   a.off = v.off;
-  for (int k = 0; k < ctx->order - 1; ++k) a.oth[k] = v.oth[k];
+  a.no = ctx->order - 1;
+  int k = 0;
+  for (int m = 0; m < ctx->order; ++m)
+    if (m != mode) {
+      a.oth[k] = v.oth[k];
+      a.U[k] = ctx->A[m];
+      ++k;
+    }
   a.val = v.val;
-  a.mask = ctx->mask;
-  for (int m = 0; m < ctx->order; ++m) a.f.U[m] = ctx->A[m];
-  a.f.order = ctx->order;
-  a.f.mode = mode;
-  a.f.rank = static_cast<int>(ctx->rank);
-  a.f.ld = static_cast<int>(ctx->ld);
+  a.mask = mask;
+  a.mode = mode;
+  a.rank = static_cast<int>(R);
   a.A = ctx->A[mode];
   a.Y = ctx->Y[mode];
-  a.row_begin = row_begin;
-  a.row_end = row_end;
+  a.items = pl.d_items;
+  a.n_items = pl.n_items;
+  a.fins = pl.d_fins;
+  a.n_fins = pl.n_fins;
+  a.partial = ctx->partial;
   a.c = cfg.c;
   a.lambda = cfg.lambda;
   a.power_tol = cfg.power_tol;
   a.power_iters = cfg.power_iters;
   a.counters = ctx->counters;
-  const int RP = static_cast<int>((ctx->rank + 1 + 3) / 4 * 4);
-  const uint64_t rows = row_end - row_begin;
-  switch (RP) {
-#define NTCB_RP(x) \
+  // reset the work cursor
+  NTCB_CUDA(cudaMemsetAsync(ctx->counters + 2, 0, sizeof(unsigned long long), ctx->stream));
+  const int LD4 = static_cast<int>(ctx->ld / 4);
+  switch (LD4) {
+#define NTCB_LD(x) \
   case x:          \
-    launch_rp<x>(ctx, a, rows); \
-    break;
-    NTCB_RP(4) NTCB_RP(8) NTCB_RP(12) NTCB_RP(16) NTCB_RP(20) NTCB_RP(24) NTCB_RP(28)
-    NTCB_RP(32) NTCB_RP(36) NTCB_RP(40) NTCB_RP(44) NTCB_RP(48) NTCB_RP(52) NTCB_RP(56)
-    NTCB_RP(60) NTCB_RP(64) NTCB_RP(68)
-#undef NTCB_RP
+    return launch_ld<x>(ctx, a, pl);
+    NTCB_LD(1) NTCB_LD(2) NTCB_LD(3) NTCB_LD(4) NTCB_LD(5) NTCB_LD(6) NTCB_LD(7) NTCB_LD(8)
+    NTCB_LD(9) NTCB_LD(10) NTCB_LD(11) NTCB_LD(12) NTCB_LD(13) NTCB_LD(14) NTCB_LD(15) NTCB_LD(16)
+#undef NTCB_LD
     default:
       fail(NTCB_EINVAL, "s_nmc: rank exceeds the supported maximum (64)");
   }
-  return 1;
 }
 
 }  // namespace ntcb
