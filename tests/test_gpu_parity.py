@@ -8,6 +8,8 @@ Bars (BASELINE.json north_star):
   * factors (fp32 device vs fp64 reference): relative Frobenius error
     <= TOL = 1e-4 per mode update / per AO iteration; metrics <= 1e-5.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -394,3 +396,18 @@ def test_cfg1_scale_properties(ntc):
     assert r1 < r0
     for m in range(3):
         assert np.all(ctx.get_factor(m)[0] >= 0)
+
+
+def test_cpp_host_api(ntc, tmp_path):
+    """include/ntcb.hpp: the reference's AO-sweep == s_nmc-replay property and
+    exception types, compiled with g++ against libntcb.so."""
+    import subprocess
+    from conftest import ROOT
+    exe = tmp_path / "test_api"
+    lib = os.path.join(ROOT, "paper_2109_09534_b200")
+    cmd = ["g++", "-std=c++17", "-O1", os.path.join(ROOT, "tests", "cpp", "test_api.cpp"),
+           "-I", os.path.join(ROOT, "include"), "-L", lib, "-lntcb",
+           f"-Wl,-rpath,{lib}", "-o", str(exe)]
+    subprocess.run(cmd, check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
