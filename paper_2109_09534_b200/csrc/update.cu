@@ -97,8 +97,10 @@ struct WarpSmem {
   static __host__ __device__ constexpr int ktile_words(int R) {  // Hf (R x HS)
     return ((R * (R | 1) + 3) / 4) * 4;
   }
+  // double-buffered raw batches (cp.async landing zone): [2][no+1][128] + masks [2][32]
+  static __host__ __device__ constexpr int batch_words(int no) { return 2 * (no + 1) * 128 + 64; }
   static __host__ __device__ constexpr int words(int no, int R) {
-    return stage_words(no) + ktile_words(R) + 64 * 2 * 2;  // + g, v as doubles
+    return stage_words(no) + ktile_words(R) + 64 * 2 * 2 + batch_words(no);  // + g, v doubles
   }
 };
 
@@ -215,6 +217,8 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
   float* Hf = wbase + W::stage_words(no);               // [R][HS]
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));  // [64]
   double* vv = gd + 64;                                             // [64]
+  uint32_t* rbat = reinterpret_cast<uint32_t*>(vv + 64);            // raw batches
+  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                       // [2][32]
   const bool full = a.c >= 1.0;
 
   // role of this lane: pick slot pk within a group, feature block s
@@ -252,24 +256,40 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
     // contiguous row), forms the Khatri-Rao block, the residual s = y.k - x
     // (segment sum over the pick's L lanes), the gradient block, and the
     // Gram blocks (s, s+d) with partner blocks fetched by shuffle.
-    auto process_group = [&](int np) {
+    // A group's gather (load_group) is issued one group ahead of its
+    // arithmetic (compute_group) so the L2 latency of the factor rows hides
+    // behind the previous group's Gram update.
+    struct Raw {
+      float4 f[NO];
+      float x;
+    };
+    auto load_group = [&](int at, int np) {
+      Raw g;
       const bool on = lane_on && pk < np;
-      const int sidx = (head + pk) & (W::kStage - 1);
-      float4 kb = make_float4(0.f, 0.f, 0.f, 0.f);
-      float x = 0.f;
-      if (on) {
-        x = st_x[sidx];
-        kb = __ldg(reinterpret_cast<const float4*>(a.U[0] + static_cast<uint64_t>(st_o[sidx]) * ld) + s);
+      const int sidx = (at + pk) & (W::kStage - 1);
 #pragma unroll
-        for (int m = 1; m < NO; ++m) {
-          if (m < no) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(
-                                       a.U[m] + static_cast<uint64_t>(st_o[m * W::kStage + sidx]) * ld) + s);
-            kb.x *= v.x;
-            kb.y *= v.y;
-            kb.z *= v.z;
-            kb.w *= v.w;
-          }
+      for (int m = 0; m < NO; ++m) g.f[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+      g.x = 0.f;
+      if (on) {
+        g.x = st_x[sidx];
+#pragma unroll
+        for (int m = 0; m < NO; ++m)
+          if (m < no)
+            g.f[m] = __ldg(reinterpret_cast<const float4*>(
+                               a.U[m] + static_cast<uint64_t>(st_o[m * W::kStage + sidx]) * ld) + s);
+      }
+      return g;
+    };
+    auto compute_group = [&](const Raw& g, int np) {
+      const bool on = lane_on && pk < np;
+      float4 kb = g.f[0];
+#pragma unroll
+      for (int m = 1; m < NO; ++m) {
+        if (m < no) {
+          kb.x *= g.f[m].x;
+          kb.y *= g.f[m].y;
+          kb.z *= g.f[m].z;
+          kb.w *= g.f[m].w;
         }
       }
       float dp = ys.x * kb.x;
@@ -280,7 +300,7 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       const int base = (lane_on ? pk : 0) * L;
 #pragma unroll
       for (int t = 0; t < L; ++t) dot += __shfl_sync(0xffffffffu, dp, base + t);
-      const float sres = on ? dot - x : 0.f;
+      const float sres = on ? dot - g.x : 0.f;
       gl.x = fmaf(sres, kb.x, gl.x);
       gl.y = fmaf(sres, kb.y, gl.y);
       gl.z = fmaf(sres, kb.z, gl.z);
@@ -302,39 +322,86 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
           kp[3] = __shfl_sync(0xffffffffu, kb.w, src);
         }
         if (d == ND - 1 && skip_last) continue;
+        if (d == 0) {  // diagonal block: upper triangle only (mirrored on output)
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+          for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c2 = 0; c2 < 4; ++c2) acc[d][4 * r + c2] = fmaf(ka[r], kp[c2], acc[d][4 * r + c2]);
+            for (int c2 = r; c2 < 4; ++c2) acc[0][4 * r + c2] = fmaf(ka[r], kp[c2], acc[0][4 * r + c2]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c2 = 0; c2 < 4; ++c2) acc[d][4 * r + c2] = fmaf(ka[r], kp[c2], acc[d][4 * r + c2]);
+        }
       }
-      head = (head + np) & (W::kStage - 1);
-      cnt -= np;
+    };
+    // all full groups currently staged, software-pipelined one group deep
+    // (ping-pong registers: no copies that would wait on in-flight loads)
+    auto drain = [&](bool flush) {
+      const int ng = cnt / GP;
+      const int rem = cnt - ng * GP;
+      const int total_g = ng + ((flush && rem > 0) ? 1 : 0);
+      if (total_g == 0) return;
+      int at = head;
+      Raw ra = load_group(at, ng > 0 ? GP : rem);
+      for (int g = 0; g < total_g; g += 2) {
+        const int npa = g < ng ? GP : rem;
+        Raw rb;
+        const bool hb = g + 1 < total_g;
+        const int npb = g + 1 < ng ? GP : rem;
+        if (hb) rb = load_group((at + npa) & (W::kStage - 1), npb);
+        compute_group(ra, npa);
+        at = (at + npa) & (W::kStage - 1);
+        if (hb) {
+          if (g + 2 < total_g) ra = load_group((at + npb) & (W::kStage - 1), g + 2 < ng ? GP : rem);
+          compute_group(rb, npb);
+          at = (at + npb) & (W::kStage - 1);
+        }
+      }
+      const int used = ng * GP + ((flush && rem > 0) ? rem : 0);
+      head = (head + used) & (W::kStage - 1);
+      cnt -= used;
     };
 
     // ---- stream the item in batches of 128 entries (4 per lane, 128-bit
     // loads issued independently of the mask), prefetching the next batch
     // while the current one is compacted and processed ----
     const uint64_t tb = w.e0 & ~uint64_t(3);  // 16-byte aligned start
-    uint4 nxo[NO], nxv;
-    uint32_t nxm = 0xffffffffu;
-    auto fetch = [&](uint64_t t) {
+    auto fetch_async = [&](uint64_t t, int buf) {
       const uint64_t e = t + 4 * lane;
       if (e < w.e1) {
 #pragma unroll
-        for (int m = 0; m < NO; ++m)
-          if (m < no) nxo[m] = __ldg(reinterpret_cast<const uint4*>(a.oth[m] + e));
-        nxv = __ldg(reinterpret_cast<const uint4*>(a.val + e));
-        if (!full) nxm = __ldg(&a.mask[e >> 5]);
+        for (int m = 0; m < NO + 1; ++m) {
+          if (m < no || m == NO) {
+            const int row = (m == NO) ? no : m;
+            const void* src = (m == NO) ? static_cast<const void*>(a.val + e) : static_cast<const void*>(a.oth[m] + e);
+            const unsigned dst = static_cast<unsigned>(
+                __cvta_generic_to_shared(rbat + (buf * (no + 1) + row) * 128 + 4 * lane));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+          }
+        }
+        if (!full) {
+          const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + lane));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dm), "l"(a.mask + (e >> 5)));
+        }
       }
+      asm volatile("cp.async.commit_group;\n" ::);
     };
-    fetch(tb);
-    for (uint64_t t0 = tb; t0 < w.e1; t0 += 128) {
+    fetch_async(tb, 0);
+    int buf = 0;
+    for (uint64_t t0 = tb; t0 < w.e1; t0 += 128, buf ^= 1) {
+      if (t0 + 128 < w.e1) {
+        fetch_async(t0 + 128, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
       uint4 co[NO];
 #pragma unroll
-      for (int m = 0; m < NO; ++m) co[m] = nxo[m];
-      const uint4 cv = nxv;
-      const uint32_t cm = nxm;
-      if (t0 + 128 < w.e1) fetch(t0 + 128);
+      for (int m = 0; m < NO; ++m)
+        if (m < no) co[m] = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + m) * 128)[lane];
+      const uint4 cv = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + no) * 128)[lane];
+      const uint32_t cm = full ? 0xffffffffu : rmsk[buf * 32 + lane];
       const uint64_t e = t0 + 4 * lane;
       uint32_t bits = full ? 0xfu : (cm >> (e & 31u)) & 0xfu;
 #pragma unroll
@@ -362,12 +429,12 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       cnt += total;
       __syncwarp();
-      while (cnt >= GP) process_group(GP);
+      drain(false);
     }
-    if (cnt > 0) process_group(cnt);
+    drain(true);
 
     // ---- reduce over the GP pick slots (lanes with equal role s) ----------
-#pragma unroll
+#pragma unroll 1
     for (int t = 1; t < GP; ++t) {
       const int src = (lane + t * L) & 31;
 #pragma unroll
@@ -397,6 +464,7 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
 #pragma unroll
         for (int e2 = 0; e2 < 16; ++e2) {
           const int row = 4 * s + (e2 >> 2), col = 4 * cb + (e2 & 3);
+          if (d == 0 && (e2 >> 2) > (e2 & 3)) continue;  // diagonal block: upper half only
           if (row < R && col < R) {
             Hf[row * HS + col] = acc[d][e2];
             Hf[col * HS + row] = acc[d][e2];
