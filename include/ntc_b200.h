@@ -171,6 +171,12 @@ int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
                      uint64_t row_begin, uint64_t row_end, uint64_t* pick_offsets,
                      uint32_t* picks);
 
+/* The production sampled-set path used by the update (mask of the picks of
+ * every row in [row_begin, row_end) for the row streams
+ * RngStream(rng_state).fork(l).fork(p)): copies the mask words covering the
+ * rows' entries, word (off[row_begin] >> 5) first, into mask_words. */
+int ntcb_sample_mask(ntcb_context* ctx, int mode, double c, uint64_t rng_state, uint64_t l,
+                     uint64_t row_begin, uint64_t row_end, uint32_t* mask_words);
 /* ntc::sample_row(view, row, c, RngStream(row_state)) (nmc.hpp:45,
  * nmc.cpp:110-118): one row, the stream used as is.  *count receives
  * floor(c * n); picks (capacity >= slice length) may be NULL to query. */

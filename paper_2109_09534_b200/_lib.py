@@ -98,6 +98,8 @@ SIGNATURES = {
     "ntcb_collect": (C.c_int, [C.c_void_p, u64p]),
     "ntcb_sample_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
                                    C.c_uint64, C.c_uint64, u64p, u32p]),
+    "ntcb_sample_mask": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
+                                   C.c_uint64, C.c_uint64, u32p]),
     "ntcb_sample_row": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_uint64, u32p,
                                   u64p]),
     "ntcb_sweep_async": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(NmcConfigC), C.c_uint64]),

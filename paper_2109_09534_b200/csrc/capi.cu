@@ -19,6 +19,12 @@ int launch_sample(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mo
                   uint32_t* dbg_picks, const uint64_t* dbg_off, int direct = 0);
 int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
                   const ntcb_nmc_config& cfg, const uint32_t* mask);
+int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
+                      uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
+                      uint64_t* heavy_cap);
+int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
+                        uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
+                        uint64_t cap);
 void free_views(ntcb_context* ctx);
 void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                      const uint32_t* h_idx, const double* h_vals);
@@ -133,7 +139,9 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
       const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
       NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->side));
       prof_mark(ctx, 1, ctx->side);
-      ctx->prof.launches += launch_sample(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, nullptr, nullptr);
+      uint64_t cap = 0;
+      ctx->prof.launches += launch_sample_set(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, &cap);
+      ctx->prof.launches += launch_sample_heavy(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, cap);
       prof_end(ctx, ctx->side);
       NTCB_CUDA(cudaEventRecord(ctx->ev_sampled[mode][par], ctx->side));
       NTCB_CUDA(cudaStreamWaitEvent(st, ctx->ev_sampled[mode][par], 0));
@@ -619,6 +627,31 @@ int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_
   NTCB_CUDA(cudaMemcpy(picks, d_pk, sizeof(uint32_t) * b, cudaMemcpyDeviceToHost));
   cudaFree(d_po);
   cudaFree(d_pk);
+  API_CATCH
+}
+
+int ntcb_sample_mask(ntcb_context* ctx, int mode, double c, uint64_t rng_state, uint64_t l,
+                     uint64_t row_begin, uint64_t row_end, uint32_t* mask_words) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "sample_mask: mode out of range");
+  if (row_begin > row_end || row_end > ctx->dims[mode])
+    fail(NTCB_ERANGE, "sample_mask: rows out of range");
+  if (!(c > 0.0 && c < 1.0)) fail(NTCB_EINVAL, "sample_mask: c must be in (0, 1)");
+  collect(ctx, nullptr);
+  const uint64_t* off = ctx->views[mode].h_off;
+  const uint64_t e0 = off[row_begin], e1 = off[row_end];
+  if (e1 <= e0) return NTCB_OK;
+  uint32_t* mask = ctx->mask[mode][0];
+  const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
+  NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));
+  uint64_t cap = 0;
+  const uint64_t root = fork64(rng_state, l);
+  launch_sample_set(ctx, ctx->stream, mask, mode, row_begin, row_end, c, root, 0, &cap);
+  launch_sample_heavy(ctx, ctx->stream, mask, mode, row_begin, row_end, c, root, 0, cap);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  NTCB_CUDA(cudaMemcpy(mask_words, mask + w0, sizeof(uint32_t) * (w1 - w0), cudaMemcpyDeviceToHost));
   API_CATCH
 }
 

@@ -120,6 +120,8 @@ struct ntcb_context {
   uint64_t partial_n = 0;
   uint32_t* perm_scratch = nullptr;  // per-entry Fisher-Yates scratch for slices too big for smem
   uint64_t perm_scratch_n = 0;
+  int* heavy_flags = nullptr;  // per heavy slice: a draw may need Lemire rejection
+  uint32_t heavy_flags_n = 0;
   unsigned long long* counters = nullptr;  // [1] first error key, [2] work cursor
   unsigned long long* h_counters = nullptr;  // pinned mirror
   double* red = nullptr;  // metrics partials

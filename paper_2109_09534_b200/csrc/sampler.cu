@@ -27,6 +27,12 @@
 //
 // Output: one bit per view entry in `mask` (the sampled SET that the update
 // kernel streams) and optionally the picks in draw order (parity tests).
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <vector>
+
 #include "common.cuh"
 
 namespace ntcb {
@@ -200,6 +206,372 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(SampleArgs a) {
       __syncwarp();
       fy_slice<uint32_t, false>(gp, n, b, state, lane, tgt, rtmp, nullptr, a.mask, beg, dbg);
       __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Production sampler: the sampled SET without the swap chain.
+//
+// For a slice of n entries with b = floor(c*n) draws r_j (j < b), let
+//   T[t] = 1 + max{ j : r_j = t, j != t }   (0 when no such j).
+// Because r_j >= j, a position t is only ever written by steps j <= t, so
+// T[t] - 1 is the last step that moved a value INTO position t before step t
+// and f(t) = T[t] ? f(T[t]-1) : t is the value sitting at position t when
+// step t runs (chains strictly decrease).  The final content of positions
+// [b, n) is the unpicked set, which gives
+//   value t >= b is picked  <=>  T[t] != 0          (it was swapped out)
+//   value v <  b is picked  <=>  v is not f(T[t]-1) for a targeted t >= b.
+// Phase 1 only STORES T (highest lane wins within a chunk, program order
+// across chunks), so there is no read-modify-write chain between chunks.
+// Phase 2 marks the unpicked roots with a flag bit in T and emits the mask.
+// Verified against the partial Fisher-Yates on 3000 random slices and by
+// tests/test_gpu_parity.py::test_production_mask_equals_pick_sets.
+// A chunk whose Lemire product might need the rejection loop switches the
+// slice to an exact serial replay of the draws on lane 0.
+// ---------------------------------------------------------------------------
+// u16 / u32 max-store with the rare intra-instruction duplicate fixed up by CAS
+__device__ __forceinline__ void tmax(uint16_t* T, uint32_t r, uint32_t v) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(T + r) & ~uintptr_t(3));
+  const uint32_t sh = (reinterpret_cast<uintptr_t>(T + r) & 2u) ? 16u : 0u;
+  uint32_t old = *w;
+  while (((old >> sh) & 0xffffu) < v) {
+    const uint32_t nw = (old & ~(0xffffu << sh)) | (v << sh);
+    const uint32_t got = atomicCAS(w, old, nw);
+    if (got == old) break;
+    old = got;
+  }
+}
+__device__ __forceinline__ void tmax(uint32_t* T, uint32_t r, uint32_t v) { atomicMax(T + r, v); }
+
+template <typename TT>
+__global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) {
+  constexpr uint32_t FLAG = 1u << (8 * sizeof(TT) - 1);
+  constexpr uint32_t VAL = FLAG - 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  TT* T = reinterpret_cast<TT*>(smem + static_cast<size_t>(wib) * a.warp_bytes);
+  if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+  const uint64_t lane_off = static_cast<uint64_t>(lane + 1) * kGolden;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kSampleWarps;
+  for (uint64_t p = a.row_begin + blockIdx.x * kSampleWarps + wib; p < a.row_end; p += nw) {
+    const uint64_t beg = a.off[p];
+    const uint32_t n = static_cast<uint32_t>(a.off[p + 1] - beg);
+    const uint32_t b = static_cast<uint32_t>(blocksize_for(a.c, n));
+    if (b == 0 || a.c >= 1.0 || n > a.cap) continue;  // skipped / full / heavy slices
+    const uint64_t state0 = a.direct ? a.root : fork64(a.root, p);
+    {
+      const uint32_t pw = (n * static_cast<uint32_t>(sizeof(TT)) + 15) / 16;
+      uint4* t4 = reinterpret_cast<uint4*>(T);
+      for (uint32_t w = lane; w < pw; w += 32) t4[w] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    // ---- phase 1: draws (64 per step), last-writer stores ---------------------
+    bool exact = false;
+    uint64_t state = state0;
+    for (uint32_t j0 = 0; j0 < b; j0 += 64) {
+      uint32_t r[2], jj[2];
+      bool act[2], ok = true;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        jj[h] = j0 + 32 * h + lane;
+        act[h] = jj[h] < b;
+        const uint32_t bound = act[h] ? n - jj[h] : 1u;
+        const uint64_t x = mix64(state + lane_off + static_cast<uint64_t>(32 * h) * kGolden);
+        const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
+        const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
+        ok = ok && !(act[h] && static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound);
+        r[h] = jj[h] + static_cast<uint32_t>(u >> 32);
+      }
+      if (__any_sync(kFull, !ok)) {
+        exact = true;
+        break;
+      }
+      state += 64 * kGolden;
+      if (act[0] && r[0] != jj[0]) T[r[0]] = static_cast<TT>(jj[0] + 1);
+      __syncwarp();
+      if (act[1] && r[1] != jj[1]) T[r[1]] = static_cast<TT>(jj[1] + 1);
+      __syncwarp();
+      // two lanes of one store instruction with the same target: keep the max
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (act[h] && r[h] != jj[h] && static_cast<uint32_t>(T[r[h]]) < jj[h] + 1) tmax(T, r[h], jj[h] + 1);
+      __syncwarp();
+    }
+    if (exact) {  // rare: replay every draw exactly (rng.hpp:32-45) on lane 0
+      __syncwarp();
+      const uint32_t pw = (n * static_cast<uint32_t>(sizeof(TT)) + 15) / 16;
+      uint4* t4 = reinterpret_cast<uint4*>(T);
+      for (uint32_t w = lane; w < pw; w += 32) t4[w] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      if (lane == 0) {
+        uint64_t s = state0;
+        for (uint32_t j = 0; j < b; ++j) {
+          const uint64_t bd = n - j;
+          s += kGolden;
+          uint64_t xx = mix64(s);
+          uint64_t l2 = xx * bd, h2 = __umul64hi(xx, bd);
+          if (l2 < bd) {
+            const uint64_t th = (0 - bd) % bd;
+            while (l2 < th) {
+              s += kGolden;
+              xx = mix64(s);
+              l2 = xx * bd;
+              h2 = __umul64hi(xx, bd);
+            }
+          }
+          const uint32_t r = j + static_cast<uint32_t>(h2);
+          if (r != j) T[r] = static_cast<TT>(j + 1);
+        }
+      }
+      __syncwarp();
+    }
+    // ---- phase 2a: positions t in [b, n): bit t; mark unpicked roots -------
+    // word k of the slice covers relative positions [32k - off0, 32k - off0 + 32)
+    uint32_t* gm = a.mask + (beg >> 5);
+    const int off0 = static_cast<int>(beg & 31u);
+    const int kb0 = (static_cast<int>(b) + off0) >> 5;
+    const int kend = (static_cast<int>(n) + off0 - 1) >> 5;
+    if (b < n) {
+      for (int k = kb0; k <= kend; ++k) {
+        const int t = 32 * k - off0 + lane;
+        const bool valid = t >= static_cast<int>(b) && t < static_cast<int>(n);
+        const uint32_t tv = valid ? (static_cast<uint32_t>(T[t]) & VAL) : 0u;
+        if (tv) {
+          uint32_t v = tv - 1, nx;
+          while ((nx = static_cast<uint32_t>(T[v]) & VAL) != 0u) v = nx - 1;
+          T[v] = static_cast<TT>(FLAG);  // roots hold 0: the flag alone
+        }
+        const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+        if (lane == 0) {
+          const bool whole = 32 * k - off0 >= static_cast<int>(b) && 32 * k - off0 + 32 <= static_cast<int>(n);
+          if (whole)
+            gm[k] = bits;
+          else if (bits)
+            atomicOr(&gm[k], bits);
+        }
+      }
+    }
+    __syncwarp();
+    // ---- phase 2b: values v in [0, b): picked unless flagged ---------------
+    const int kbend = (static_cast<int>(b) + off0 - 1) >> 5;
+    for (int k = 0; k <= kbend; ++k) {
+      const int t = 32 * k - off0 + lane;
+      const bool pick = t >= 0 && t < static_cast<int>(b) && !(static_cast<uint32_t>(T[t]) & FLAG);
+      const uint32_t bits = __ballot_sync(kFull, pick);
+      if (lane == 0) {
+        const bool whole = 32 * k - off0 >= 0 && 32 * k - off0 + 32 <= static_cast<int>(b);
+        if (whole)
+          gm[k] = bits;
+        else if (bits)
+          atomicOr(&gm[k], bits);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
+                      uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
+                      uint64_t* heavy_cap) {
+  const DeviceView& v = ctx->views[mode];
+  if (row_end <= row_begin) return 0;
+  if (v.max_slice >= (1ull << 31))
+    fail(NTCB_EINVAL, "sampler: slices of 2^31 or more entries are not supported");
+  SampleArgs a{};
+  a.off = v.off;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.c = c;
+  a.root = root;
+  a.mask = mask;
+  a.counters = ctx->counters;
+  a.direct = direct;
+  const uint64_t maxn = v.max_slice;
+  const bool small = maxn <= 32767;
+  const uint64_t esz = small ? 2 : 4;
+  uint64_t cap = maxn;
+  const uint64_t budget = 56 * 1024;
+  if (cap * esz > budget) cap = budget / esz;
+  if (cap < 32) cap = 32;
+  a.cap = cap;
+  a.warp_bytes = static_cast<uint32_t>((cap * esz + 15) / 16 * 16);
+  if (heavy_cap) *heavy_cap = cap;
+  const size_t smem = static_cast<size_t>(a.warp_bytes) * kSampleWarps;
+  int per_sm = 0;
+  auto kern = small ? k_sample_set<uint16_t> : k_sample_set<uint32_t>;
+  NTCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSampleWarps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t rows = row_end - row_begin;
+  uint64_t grid = (rows + kSampleWarps - 1) / kSampleWarps;
+  grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+  kern<<<static_cast<unsigned>(grid), kSampleWarps * 32, smem, stream>>>(a);
+  NTCB_CUDA(cudaGetLastError());
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// Heavy slices (n above the per-warp shared-memory budget): the same set
+// formulation over the whole grid.  T lives in the per-entry u32 scratch
+// (T[t] of slice p at scratch[beg + t], flag bit 31); kernel boundaries are
+// the phase barriers; last-writer becomes atomicMax.  Slices where a draw
+// might need Lemire's rejection loop are flagged and redone by the exact
+// ordered warp sampler (fy_slice on the global scratch).
+// ---------------------------------------------------------------------------
+struct HeavyRow {
+  uint64_t row, beg;
+  uint32_t n, b;
+};
+
+__global__ void k_heavy_zero(const HeavyRow* rows, uint32_t* scratch, int* flags) {
+  const HeavyRow h = rows[blockIdx.y];
+  if (blockIdx.x == 0 && threadIdx.x == 0) flags[blockIdx.y] = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < h.n; t += gridDim.x * blockDim.x)
+    scratch[h.beg + t] = 0u;
+}
+
+__global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags, uint64_t root,
+                             int direct) {
+  const HeavyRow h = rows[blockIdx.y];
+  const uint64_t state = direct ? root : fork64(root, h.row);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < h.b; j += gridDim.x * blockDim.x) {
+    const uint32_t bound = h.n - j;
+    const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
+    const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
+    const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
+    if (static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound) flags[blockIdx.y] = 1;
+    const uint32_t r = j + static_cast<uint32_t>(u >> 32);
+    if (r != j) atomicMax(&scratch[h.beg + r], j + 1);
+  }
+}
+
+__global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int* flags,
+                             uint32_t* mask) {
+  const HeavyRow h = rows[blockIdx.y];
+  if (flags[blockIdx.y]) return;
+  const uint64_t gb0 = h.beg + h.b, gb1 = h.beg + h.n;
+  if (gb1 <= gb0) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = gb0 >> 5, w1 = (gb1 - 1) >> 5;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
+    const uint64_t g = (w << 5) + lane;
+    const bool valid = g >= gb0 && g < gb1;
+    const uint32_t tv = valid ? (scratch[g] & 0x7fffffffu) : 0u;
+    if (tv) {
+      uint32_t v = tv - 1, nx;
+      while ((nx = scratch[h.beg + v] & 0x7fffffffu) != 0u) v = nx - 1;
+      scratch[h.beg + v] = 0x80000000u;  // unpicked root
+    }
+    const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+    if (lane == 0) {
+      if ((w << 5) >= gb0 && (w << 5) + 32 <= gb1)
+        mask[w] = bits;
+      else if (bits)
+        atomicOr(&mask[w], bits);
+    }
+  }
+}
+
+__global__ void k_heavy_head(const HeavyRow* rows, const uint32_t* scratch, const int* flags,
+                             uint32_t* mask) {
+  const HeavyRow h = rows[blockIdx.y];
+  if (flags[blockIdx.y] || h.b == 0) return;
+  const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
+    const uint64_t g = (w << 5) + lane;
+    const bool pick = g >= ga0 && g < ga1 && !(scratch[g] & 0x80000000u);
+    const uint32_t bits = __ballot_sync(kFull, pick);
+    if (lane == 0) {
+      if ((w << 5) >= ga0 && (w << 5) + 32 <= ga1)
+        mask[w] = bits;
+      else if (bits)
+        atomicOr(&mask[w], bits);
+    }
+  }
+}
+
+// exact ordered fallback for flagged heavy slices (one warp each)
+__global__ void k_heavy_exact(const HeavyRow* rows, uint32_t* scratch, const int* flags,
+                              uint32_t* mask, uint64_t root, int direct) {
+  __shared__ int tgt[32];
+  __shared__ uint32_t rtmp[32];
+  const HeavyRow h = rows[blockIdx.x];
+  if (!flags[blockIdx.x]) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t* gp = scratch + h.beg;
+  for (uint32_t t = lane; t < h.n; t += 32) gp[t] = 0u;
+  __syncwarp();
+  fy_slice<uint32_t, false>(gp, h.n, h.b, direct ? root : fork64(root, h.row), lane, tgt, rtmp,
+                            nullptr, mask, h.beg, nullptr);
+}
+
+static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>,
+                std::pair<HeavyRow*, uint32_t>> g_heavy;
+
+int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
+                        uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
+                        uint64_t cap) {
+  const DeviceView& v = ctx->views[mode];
+  if (v.max_slice <= cap || c >= 1.0) return 0;
+  uint64_t cbits;
+  std::memcpy(&cbits, &c, 8);
+  auto key = std::make_tuple(static_cast<const void*>(v.off), row_begin, row_end, cbits, cap);
+  auto it = g_heavy.find(key);
+  if (it == g_heavy.end()) {
+    std::vector<HeavyRow> hr;
+    uint32_t maxn = 0;
+    for (uint64_t p = row_begin; p < row_end; ++p) {
+      const uint64_t n = v.h_off[p + 1] - v.h_off[p];
+      const uint64_t b = blocksize_for(c, n);
+      if (n > cap && b > 0) {
+        hr.push_back({p, v.h_off[p], static_cast<uint32_t>(n), static_cast<uint32_t>(b)});
+        maxn = std::max<uint32_t>(maxn, static_cast<uint32_t>(n));
+      }
+    }
+    HeavyRow* d = nullptr;
+    if (!hr.empty()) {
+      NTCB_CUDA(cudaMalloc(&d, sizeof(HeavyRow) * (hr.size() + 1)));
+      NTCB_CUDA(cudaMemcpy(d, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
+    }
+    it = g_heavy.emplace(key, std::make_pair(d, static_cast<uint32_t>(hr.size()))).first;
+    (void)maxn;
+  }
+  const uint32_t nh = it->second.second;
+  if (nh == 0) return 0;
+  if (nh > 65535) fail(NTCB_EINVAL, "sampler: more than 65535 heavy slices in one call");
+  if (!ctx->perm_scratch) fail(NTCB_ECUDA, "sampler: heavy slices need the per-entry scratch");
+  if (ctx->heavy_flags_n < nh) {
+    if (ctx->heavy_flags) cudaFree(ctx->heavy_flags);
+    NTCB_CUDA(cudaMalloc(&ctx->heavy_flags, sizeof(int) * nh));
+    ctx->heavy_flags_n = nh;
+  }
+  const HeavyRow* d = it->second.first;
+  const dim3 grid(static_cast<unsigned>(ctx->sm_count * 2), nh);
+  k_heavy_zero<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
+  k_heavy_draw<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
+  k_heavy_tail<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  k_heavy_head<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  k_heavy_exact<<<nh, 32, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask, root, direct);
+  NTCB_CUDA(cudaGetLastError());
+  return 5;
+}
+
+void drop_heavy(ntcb_context* ctx) {
+  for (auto it = g_heavy.begin(); it != g_heavy.end();) {
+    bool mine = false;
+    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
+      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
+    if (mine) {
+      if (it->second.first) cudaFree(it->second.first);
+      it = g_heavy.erase(it);
+    } else {
+      ++it;
     }
   }
 }

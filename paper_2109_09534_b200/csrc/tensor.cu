@@ -171,9 +171,11 @@ void radix_pairs(ntcb_context* ctx, KT* keys, KT* keys_alt, uint32_t* vals, uint
 }  // namespace
 
 void drop_plans(ntcb_context* ctx);
+void drop_heavy(ntcb_context* ctx);
 
 void free_views(ntcb_context* ctx) {
   drop_plans(ctx);
+  drop_heavy(ctx);
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
     DeviceView& v = ctx->views[m];
     if (v.off) cudaFree(v.off);
@@ -194,6 +196,9 @@ void free_views(ntcb_context* ctx) {
   ctx->partial_n = 0;
   if (ctx->perm_scratch) cudaFree(ctx->perm_scratch);
   ctx->perm_scratch = nullptr;
+  if (ctx->heavy_flags) cudaFree(ctx->heavy_flags);
+  ctx->heavy_flags = nullptr;
+  ctx->heavy_flags_n = 0;
   ctx->perm_scratch_n = 0;
   ctx->nnz = 0;
   ctx->order = 0;
@@ -309,7 +314,7 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
   // Per-entry Fisher-Yates scratch for slices beyond the sampler's smem budget.
   uint64_t big = 0;
   for (int m = 0; m < order; ++m) big = std::max(big, ctx->views[m].max_slice);
-  if (big > 8192) {
+  if (big > 4096) {
     ctx->perm_scratch_n = nnz;
     NTCB_CUDA(cudaMalloc(&ctx->perm_scratch, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)));
   }

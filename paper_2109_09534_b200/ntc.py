@@ -343,6 +343,21 @@ class Context:
                                       po.ctypes.data_as(u64p), picks.ctypes.data_as(u32p)))
         return po, picks[: int(po[-1])]
 
+    def sample_mask(self, mode, c, rng_state, l=0, row_begin=0, row_end=None):
+        """Production sampled-set mask for rows [row_begin, row_end): returns
+        (first entry position e0, boolean array over entries [e0, e1))."""
+        off = self.view_offsets(mode)
+        row_end = len(off) - 1 if row_end is None else row_end
+        e0, e1 = int(off[row_begin]), int(off[row_end])
+        if e1 <= e0:
+            return e0, np.zeros(0, bool)
+        w0, w1 = e0 >> 5, ((e1 - 1) >> 5) + 1
+        words = np.zeros(w1 - w0, np.uint32)
+        check(self.L.ntcb_sample_mask(self.h, mode, c, rng_state, l, row_begin, row_end,
+                                      words.ctypes.data_as(u32p)))
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little").astype(bool)
+        return e0, bits[e0 - 32 * w0: e1 - 32 * w0]
+
     def sample_row(self, mode, row, c, row_state):
         cnt = C.c_uint64()
         check(self.L.ntcb_sample_row(self.h, mode, row, c, row_state, None, C.byref(cnt)))

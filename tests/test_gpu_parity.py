@@ -411,3 +411,28 @@ def test_cpp_host_api(ntc, tmp_path):
     subprocess.run(cmd, check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("lens", [(37, 1000, 9000, 23000), (40000, 12000, 3), (90000, 70000, 5, 14000)])
+def test_production_mask_equals_pick_sets(ntc, orc, lens):
+    """The update kernel's sampled set (k_sample_set / heavy-slice path) is
+    exactly the set of the reference's partial Fisher-Yates picks."""
+    rows = len(lens)
+    width = max(lens)
+    rng = np.random.default_rng(sum(lens))
+    idx = []
+    for p, n in enumerate(lens):
+        cols = np.sort(rng.choice(width, n, replace=False))
+        idx.append(np.stack([np.full(n, p), cols], 1))
+    idx = np.concatenate(idx).astype(np.uint32)
+    c = ctx_for(ntc, [rows, width], idx, np.ones(len(idx), np.float32))
+    off = c.view_offsets(0)
+    for cf in (0.5, 0.93, 0.02):
+        st = 0xBEEF + len(idx)
+        e0, bits = c.sample_mask(0, cf, st, 1)
+        for p in range(rows):
+            n = int(off[p + 1] - off[p])
+            want = np.zeros(n, bool)
+            want[orc.sample_row(n, cf, orc.fork(orc.fork(st, 1), p))] = True
+            got = bits[int(off[p]) - e0: int(off[p + 1]) - e0]
+            np.testing.assert_array_equal(got, want)
