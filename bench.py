@@ -35,14 +35,27 @@ SEED_SOLVER = 7
 CONFIGS = {
     1: dict(dims=[500, 500, 500], nnz=1_250_000, true_rank=10, sigma=0.01, R=10, iters=20),
     2: dict(dims=[10000, 10000, 10000], nnz=100_000_000, true_rank=20, sigma=0.01, R=20, iters=10),
+    # Zipf(1.2) over permuted ids on modes 0 and 1, 1-5 ratings (value_kind 1)
+    3: dict(dims=[480189, 17770, 2182], nnz=100_000_000, true_rank=10, sigma=0.5, R=16, iters=10,
+            zipf=[1.2, 1.2, 0.0], kind=1),
     4: dict(dims=[50000, 50000, 1000, 100], nnz=500_000_000, true_rank=32, sigma=0.01, R=32, iters=10),
 }
 
 
+def generate(ctx, cfgd, cid):
+    ctx.synth(cfgd["dims"], cfgd["nnz"], cfgd["true_rank"], cfgd["sigma"], 1000 + cid,
+              cfgd.get("zipf"), cfgd.get("kind", 0))
+
+
 def workload_name(cid, c):
     d = "x".join(str(x) for x in c["dims"])
-    return (f"cfg{cid}: {d}, nnz={c['nnz']}, truth rank {c['true_rank']} U[0,1) + N(0,{c['sigma']}^2) "
-            f"clamped>=0, fit rank {c['R']}, c=0.5, MAX_INNER=1, lambda=1e-3")
+    if c.get("kind", 0) == 1:
+        vals = (f"modes Zipf{tuple(c['zipf'])} over permuted ids, ratings round(clip(1+4*CPD_r{c['true_rank']}/"
+                f"{c['true_rank']} + N(0,{c['sigma']}^2), 1, 5))")
+    else:
+        vals = f"uniform cells, truth rank {c['true_rank']} U[0,1) + N(0,{c['sigma']}^2) clamped>=0"
+    return f"cfg{cid}: {d}, nnz={c['nnz']}, {vals}, fit rank {c['R']}, c=0.5, MAX_INNER=1, lambda=1e-3"
+
 
 
 def peaks():
@@ -101,17 +114,27 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU reference (oracle/_ref) on a bounded row sample of the same tensor
 # ---------------------------------------------------------------------------
-def reference_sample(ctx, cfgd, rows_per_mode, steps, threads):
+def sample_rows(ctx, order, target_per_mode=12_000_000):
+    """Per-mode row prefix whose sampled entries reach ~target (bounded CPU sample)."""
+    from paper_2109_09534_b200.dist import blocksizes
+    out = []
+    for m in range(order):
+        cum = np.cumsum(blocksizes(ctx.view_offsets(m), 0.5).astype(np.int64))
+        out.append(int(min(len(cum), np.searchsorted(cum, target_per_mode) + 1)))
+    return out
+
+
+def reference_sample(ctx, cfgd, rows, steps, threads):
     """Times the reference's s_nmc (RefProblem -> libntc_ref.so) on the first
-    `rows_per_mode` rows of every mode view of the tensor held by `ctx`
-    (row prefixes keep the reference's row streams identical to the full
-    problem).  Returns (sampled nnz/s, seconds of s_nmc, sampled, per-step s)."""
+    rows[m] rows of every mode view of the tensor held by `ctx` (row prefixes
+    keep the reference's row streams identical to the full problem).  Returns
+    (sampled nnz/s, seconds of s_nmc, sampled, per-step s)."""
     import oracle as O
     dims = cfgd["dims"]
     N, R = len(dims), cfgd["R"]
     views = []
     for m in range(N):
-        off, oth, val = ctx.view_rows(m, 0, rows_per_mode)
+        off, oth, val = ctx.view_rows(m, 0, rows[m])
         views.append((off, oth, val.astype(np.float64)))
     rp = O.RefProblem(dims, views=views)
     F = O.ref_initial_factors(dims, R, SEED_SOLVER)
@@ -123,23 +146,18 @@ def reference_sample(ctx, cfgd, rows_per_mode, steps, threads):
         t_step = 0.0
         for m in range(N):
             a, _ = rp.get_factor(m)
-            rp.set_factor_rows(m, a[:rows_per_mode])
+            rp.set_factor_rows(m, a[:rows[m]])
             t0 = time.perf_counter()
             n = rp.s_nmc(m, cfg, orc.sweep_state(SEED_SOLVER, k, m))
             dt = time.perf_counter() - t0
-            a_s, _ = rp.get_factor(m, rows_per_mode)
-            a[:rows_per_mode] = a_s
+            a_s, _ = rp.get_factor(m, rows[m])
+            a[:rows[m]] = a_s
             rp.set_factor_rows(m, a)
             t_step += dt
             tot_n += n
         per.append(t_step)
         tot_s += t_step
     return tot_n / tot_s, tot_s, tot_n, per
-
-
-def sample_rows_for(cfgd, target_per_mode=12_000_000):
-    n_per_row = cfgd["nnz"] / max(cfgd["dims"])
-    return int(max(1, min(min(cfgd["dims"]), target_per_mode / (0.5 * n_per_row))))
 
 
 def full_sampled_per_sweep(ctx, order):
@@ -153,14 +171,14 @@ def run_reference(args, cfgd, cid):
         return
     import paper_2109_09534_b200 as P
     ctx = P.Context(0)  # data generation only (device generator, bit-identical inputs)
-    ctx.synth_uniform(cfgd["dims"], cfgd["nnz"], cfgd["true_rank"], cfgd["sigma"], 1000 + cid)
+    generate(ctx, cfgd, cid)
     order = len(cfgd["dims"])
     full = full_sampled_per_sweep(ctx, order)
     threads = os.cpu_count() or 1
-    S = sample_rows_for(cfgd)
+    S = sample_rows(ctx, order)
     rate_w, _, _, _ = reference_sample(ctx, cfgd, S, args.warmup, threads) if args.warmup else (0, 0, 0, [])
     rate, secs, n, per = reference_sample(ctx, cfgd, S, args.steps, threads)
-    sample = (f"first {S} rows of each of the {order} mode views per step "
+    sample = (f"first {S} rows of the {order} mode views per step "
               f"({n // max(args.steps, 1)} sampled entries/step); s_nmc wall time only "
               f"(steady_clock convention of ao.cpp:93)")
     out = {
@@ -196,7 +214,7 @@ def run_ours(args, cfgd, cid):
     order = len(dims)
     ctx = P.Context(local)
     ctx.set_stream(stream.cuda_stream)
-    ctx.synth_uniform(dims, cfgd["nnz"], cfgd["true_rank"], cfgd["sigma"], 1000 + cid)
+    generate(ctx, cfgd, cid)
     ctx.random_factors(R, SEED_SOLVER)
     cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
     sharded = ShardedSweep(ctx, cfg, rank, world) if world > 1 else None
@@ -296,10 +314,10 @@ def run_ours(args, cfgd, cid):
     if world == 1 and not args.no_cpu:
         import oracle  # noqa: F401  (checker/baseline only)
         threads = os.cpu_count() or 1
-        S = sample_rows_for(cfgd)
+        S = sample_rows(ctx, order)
         rate, secs, n, _ = reference_sample(ctx, cfgd, S, 2, threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-               "sample": f"oracle/_ref s_nmc on the first {S} rows of each mode view, 2 sweeps, "
+               "sample": f"oracle/_ref s_nmc on the first {S} rows of the mode views, 2 sweeps, "
                          f"{n} sampled entries in {secs:.1f} s"}
 
     if rank == 0:

@@ -208,6 +208,13 @@ int ntcb_rmse(ntcb_context* ctx, double* out);
 int ntcb_synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                        uint64_t true_rank, double sigma, uint64_t seed);
 
+/* General form: zipf_alpha[m] > 0 draws mode m from Zipf(alpha) over a
+ * seeded permutation of the ids (NULL or 0 = uniform); value_kind 0 = CPD +
+ * noise clamped at 0, 1 = round(clip(1 + 4 CPD/true_rank + noise, 1, 5)). */
+int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+               uint64_t true_rank, double sigma, uint64_t seed, const double* zipf_alpha,
+               int value_kind);
+
 /* ---- timing hooks for bench.py ----------------------------------------- */
 /* Kernel-level timing of the last ntcb_collect window: total device ms of
  * the update (accumulate) kernels and of the sampler kernels, and number of

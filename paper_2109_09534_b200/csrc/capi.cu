@@ -33,6 +33,9 @@ void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_
 void device_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg);
 void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                    uint64_t true_rank, double sigma, uint64_t seed);
+void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                   uint64_t true_rank, double sigma, uint64_t seed, const double* zipf_alpha,
+                   int kind);
 }  // namespace ntcb
 
 using namespace ntcb;
@@ -366,6 +369,17 @@ int ntcb_synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint6
   need_ctx(ctx);
   free_factors(ctx);
   synth_uniform(ctx, order, dims, nnz, true_rank, sigma, seed);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+               uint64_t true_rank, double sigma, uint64_t seed, const double* zipf_alpha,
+               int value_kind) {
+  API_TRY
+  need_ctx(ctx);
+  free_factors(ctx);
+  synth_general(ctx, order, dims, nnz, true_rank, sigma, seed, zipf_alpha, value_kind);
   g_host[ctx].bs_cache.clear();
   API_CATCH
 }

@@ -1,19 +1,27 @@
 // Synthetic tensors of the BASELINE.json shapes, generated on the device.
 // (Not part of the reference: its synth_generate (synth.cpp:84-145) cannot
-// express exact-count uniform sampling at these sizes.)
+// express exact-count sampling, Zipf modes or these sizes.)
 //
-// Uniform configs: candidate cell j has coordinates
-//   i_m = hi32( hi32(mix(S_mask + (j*N + m + 1) G)) * dims[m] )
-// with S_mask = fork(fork(seed, 5), 0); candidates are taken in j order and a
-// cell already seen is redrawn (= skipped), until nnz unique cells exist.
-// Truth factors U_m[i, r] = next_double of fork(fork(seed, 4), m) at index
-// i*R + r (row-major, as FactorSet::random_uniform, factor_set.cpp:18-27);
-// value = sum_r prod_m U_m[i_m, r] + sigma * gauss_j, clamped at 0, where
-// gauss_j is the reference's Box-Muller (rng.hpp:49-53) on fork(fork(seed,6), j).
+// Candidate cell j has coordinates drawn from u_{j,m} = mix(S_mask + (j*N + m
+// + 1) G), S_mask = fork(fork(seed, 5), 0):
+//   uniform mode:  i_m = hi32( hi32(u) * dims[m] )
+//   Zipf(alpha):   rank k = first k with CDF(k) > (u >> 11) 2^-53 over
+//                  P(k) ~ (k+1)^-alpha, then i_m = perm_m[k] with perm_m a
+//                  seeded Fisher-Yates permutation of the ids (stream
+//                  fork(fork(seed, 7), m)) -- "Zipf over randomly permuted ids".
+// Candidates are taken in j order and a cell already seen is redrawn
+// (= skipped) until nnz unique cells exist.  Truth factors U_m[i, r] =
+// next_double of fork(fork(seed, 4), m) at index i*R + r (row-major, as
+// FactorSet::random_uniform, factor_set.cpp:18-27).  Values:
+//   kind 0: sum_r prod_m U_m[i_m, r] + sigma g_j, clamped at 0;
+//   kind 1: round(clip(1 + 4 * (sum_r prod_m U_m[i_m, r]) / R_true + sigma g_j, 1, 5))
+//           (the 1-5 rating model of BASELINE configs[2]);
+// g_j is the reference's Box-Muller (rng.hpp:49-53) on fork(fork(seed, 6), j).
 // Tags 4..6 follow synth.cpp:16-18.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
@@ -34,26 +42,39 @@ struct Buf {
   ~Buf() {
     if (p) cudaFree(p);
   }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
 };
 
 struct Dims {
   uint64_t d[NTCB_MAX_ORDER];
   int shift[NTCB_MAX_ORDER];
+  const double* cdf[NTCB_MAX_ORDER];     // Zipf modes: CDF over ranks (nullptr = uniform)
+  const uint32_t* perm[NTCB_MAX_ORDER];  // Zipf modes: rank -> id
   int order;
 };
 
-__device__ __forceinline__ uint32_t coord_of(uint64_t s_mask, uint64_t j, int m, int order,
-                                             uint64_t dim) {
-  const uint64_t u = mix64(s_mask + (j * order + m + 1) * kGolden);
-  return static_cast<uint32_t>(((u >> 32) * dim) >> 32);
+__device__ __forceinline__ uint32_t coord_of(const Dims& d, uint64_t s_mask, uint64_t j, int m) {
+  const uint64_t u = mix64(s_mask + (j * d.order + m + 1) * kGolden);
+  if (d.cdf[m] == nullptr) return static_cast<uint32_t>(((u >> 32) * d.d[m]) >> 32);
+  const double x = static_cast<double>(u >> 11) * 0x1.0p-53;
+  const double* cdf = d.cdf[m];
+  uint64_t lo = 0, hi = d.d[m] - 1;  // first k with cdf[k] > x (cdf[last] == 1)
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] > x)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return d.perm[m][lo];
 }
 
 __global__ void k_candidates(uint64_t s_mask, uint64_t M, Dims d, uint64_t* key, uint32_t* jj) {
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < M;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t k = 0;
-    for (int m = 0; m < d.order; ++m)
-      k |= static_cast<uint64_t>(coord_of(s_mask, j, m, d.order, d.d[m])) << d.shift[m];
+    for (int m = 0; m < d.order; ++m) k |= static_cast<uint64_t>(coord_of(d, s_mask, j, m)) << d.shift[m];
     key[j] = k;
     jj[j] = static_cast<uint32_t>(j);
   }
@@ -71,21 +92,20 @@ __global__ void k_first(const uint64_t* skey, const uint32_t* sj, uint64_t M, ui
 }
 
 __global__ void k_truth(uint64_t root, uint64_t n, double* out) {
-  // out[q] = q-th next_double of stream `root`
   for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[q] = static_cast<double>(mix64(root + (q + 1) * kGolden) >> 11) * 0x1.0p-53;
 }
 
 __global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d, int R,
-                       const double* const* truth, uint64_t noise_root, double sigma,
+                       const double* const* truth, uint64_t noise_root, double sigma, int kind,
                        uint32_t* idx, float* vals) {
   for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < nnz;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t j = js[e];
     uint32_t ix[NTCB_MAX_ORDER];
     for (int m = 0; m < d.order; ++m) {
-      ix[m] = coord_of(s_mask, j, m, d.order, d.d[m]);
+      ix[m] = coord_of(d, s_mask, j, m);
       idx[e * d.order + m] = ix[m];
     }
     double model = 0.0;
@@ -94,16 +114,24 @@ __global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d
       for (int m = 0; m < d.order; ++m) prod *= truth[m][static_cast<uint64_t>(ix[m]) * R + r];
       model += prod;
     }
-    double v = model;
+    double g = 0.0;
     if (sigma > 0.0) {
       uint64_t s = fork64(noise_root, j);
       s += kGolden;
       const double u1 = static_cast<double>((mix64(s) >> 11) + 1) * 0x1.0p-53;
       s += kGolden;
       const double u2 = static_cast<double>(mix64(s) >> 11) * 0x1.0p-53;
-      v += sigma * sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+      g = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
     }
-    vals[e] = static_cast<float>(v > 0.0 ? v : 0.0);
+    double v;
+    if (kind == 1) {
+      v = 1.0 + 4.0 * model / R + sigma * g;
+      v = rint(fmin(fmax(v, 1.0), 5.0));
+    } else {
+      v = model + sigma * g;
+      v = v > 0.0 ? v : 0.0;
+    }
+    vals[e] = static_cast<float>(v);
   }
 }
 
@@ -113,11 +141,36 @@ unsigned grid_of(uint64_t n, int sms) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(g, cap)));
 }
 
+// host splitmix64 stream (rng.hpp semantics)
+struct HostRng {
+  uint64_t s;
+  uint64_t next() {
+    s += kGolden;
+    return mix64(s);
+  }
+  uint64_t below(uint64_t bound) {  // Lemire with rejection (rng.hpp:32-45)
+    uint64_t x = next();
+    unsigned __int128 m = static_cast<unsigned __int128>(x) * bound;
+    uint64_t lo = static_cast<uint64_t>(m);
+    if (lo < bound) {
+      const uint64_t th = (0 - bound) % bound;
+      while (lo < th) {
+        x = next();
+        m = static_cast<unsigned __int128>(x) * bound;
+        lo = static_cast<uint64_t>(m);
+      }
+    }
+    return static_cast<uint64_t>(m >> 64);
+  }
+};
+
 }  // namespace
 
-void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
-                   uint64_t true_rank, double sigma, uint64_t seed) {
+void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                   uint64_t true_rank, double sigma, uint64_t seed, const double* zipf_alpha,
+                   int kind) {
   if (order < 2 || order > NTCB_MAX_ORDER) fail(NTCB_EINVAL, "synth: order must be in [2, 8]");
+  if (kind != 0 && kind != 1) fail(NTCB_EINVAL, "synth: unknown value kind");
   Dims d{};
   d.order = order;
   int bits = 0;
@@ -135,15 +188,53 @@ void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
   if (static_cast<long double>(nnz) > 0.5L * cells)
     fail(NTCB_EINVAL, "synth: nnz exceeds half the cell space");
   if (true_rank == 0 || true_rank > 256) fail(NTCB_EINVAL, "synth: bad true rank");
+  if (nnz >= (1ull << 32)) fail(NTCB_EINVAL, "synth: nnz must be < 2^32 per device");
   cudaStream_t st = ctx->stream;
   const int sms = ctx->sm_count;
   const uint64_t s_mask = fork64(fork64(seed, 5), 0);
   const uint64_t noise_root = fork64(seed, 6);
 
+  // Zipf tables: CDF over ranks and a seeded id permutation per Zipf mode
+  std::vector<double*> d_cdf(order, nullptr);
+  std::vector<uint32_t*> d_perm(order, nullptr);
+  struct Cleanup {
+    std::vector<double*>& a;
+    std::vector<uint32_t*>& b;
+    ~Cleanup() {
+      for (auto* p : a)
+        if (p) cudaFree(p);
+      for (auto* p : b)
+        if (p) cudaFree(p);
+    }
+  } cleanup{d_cdf, d_perm};
+  for (int m = 0; m < order; ++m) {
+    const double al = zipf_alpha ? zipf_alpha[m] : 0.0;
+    if (!(al > 0.0)) continue;
+    const uint64_t N = dims[m];
+    std::vector<double> cdf(N);
+    double acc = 0.0;
+    for (uint64_t k = 0; k < N; ++k) {
+      acc += std::pow(static_cast<double>(k + 1), -al);
+      cdf[k] = acc;
+    }
+    for (auto& c : cdf) c /= acc;
+    cdf[N - 1] = 1.0;
+    std::vector<uint32_t> perm(N);
+    for (uint64_t k = 0; k < N; ++k) perm[k] = static_cast<uint32_t>(k);
+    HostRng rng{fork64(fork64(seed, 7), m)};
+    for (uint64_t k = N - 1; k > 0; --k) std::swap(perm[k], perm[rng.below(k + 1)]);
+    NTCB_CUDA(cudaMalloc(&d_cdf[m], sizeof(double) * N));
+    NTCB_CUDA(cudaMalloc(&d_perm[m], sizeof(uint32_t) * N));
+    NTCB_CUDA(cudaMemcpy(d_cdf[m], cdf.data(), sizeof(double) * N, cudaMemcpyHostToDevice));
+    NTCB_CUDA(cudaMemcpy(d_perm[m], perm.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice));
+    d.cdf[m] = d_cdf[m];
+    d.perm[m] = d_perm[m];
+  }
+
   uint64_t M = nnz + std::max<uint64_t>(nnz / 256, 4096);
   Buf<uint32_t> chosen(nnz);
   for (int attempt = 0;; ++attempt) {
-    if (M >= (1ull << 32)) fail(NTCB_EINVAL, "synth: too many candidates");
+    if (M >= (1ull << 32) - 1) fail(NTCB_EINVAL, "synth: too many candidates (duplicate-heavy distribution)");
     Buf<uint64_t> key(M), key2(M);
     Buf<uint32_t> jj(M), jj2(M);
     k_candidates<<<grid_of(M, sms), 256, 0, st>>>(s_mask, M, d, key.p, jj.p);
@@ -156,7 +247,6 @@ void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
     NTCB_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, dk, dv, static_cast<int64_t>(M), 0, bits, st));
     Buf<unsigned long long> cnt(1);
     NTCB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
-    // keep_j reuses the idle u32 buffer
     uint32_t* keep = dv.Current() == jj.p ? jj2.p : jj.p;
     k_first<<<grid_of(M, sms), 256, 0, st>>>(dk.Current(), dv.Current(), M, keep, cnt.p);
     NTCB_CUDA(cudaGetLastError());
@@ -164,7 +254,9 @@ void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
     NTCB_CUDA(cudaMemcpyAsync(&uniq, cnt.p, sizeof uniq, cudaMemcpyDeviceToHost, st));
     NTCB_CUDA(cudaStreamSynchronize(st));
     if (uniq < nnz) {
-      M = M + (nnz - uniq) * 2 + 4096;
+      const double frac = static_cast<double>(uniq) / static_cast<double>(M);
+      uint64_t next = static_cast<uint64_t>(static_cast<double>(nnz) / std::max(frac, 1e-3) * 1.05) + 4096;
+      M = std::max<uint64_t>(next, M + M / 4);
       continue;
     }
     // ascending j; skipped entries carry 0xffffffff and sort last
@@ -191,11 +283,16 @@ void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
   Buf<uint32_t> idx(nnz * order);
   Buf<float> vals(nnz);
   k_emit<<<grid_of(nnz, sms), 256, 0, st>>>(chosen.p, nnz, s_mask, d, R, dtruth.p, noise_root,
-                                            sigma, idx.p, vals.p);
+                                            sigma, kind, idx.p, vals.p);
   NTCB_CUDA(cudaGetLastError());
   NTCB_CUDA(cudaStreamSynchronize(st));
   for (double* p : truth) cudaFree(p);
   load_tensor_f32(ctx, order, dims, nnz, idx.p, vals.p, true);
+}
+
+void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
+                   uint64_t true_rank, double sigma, uint64_t seed) {
+  synth_general(ctx, order, dims, nnz, true_rank, sigma, seed, nullptr, 0);
 }
 
 }  // namespace ntcb

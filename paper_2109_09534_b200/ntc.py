@@ -219,6 +219,15 @@ class Context:
         check(self.L.ntcb_synth_uniform(self.h, len(dims), dims.ctypes.data_as(u64p), nnz,
                                         true_rank, sigma, seed))
 
+    def synth(self, dims, nnz, true_rank, sigma, seed, zipf_alpha=None, value_kind=0):
+        dims = np.ascontiguousarray(dims, np.uint64)
+        za = None
+        if zipf_alpha is not None:
+            za = np.ascontiguousarray(zipf_alpha, np.float64)
+        check(self.L.ntcb_synth(self.h, len(dims), dims.ctypes.data_as(u64p), nnz, true_rank,
+                                sigma, seed, None if za is None else za.ctypes.data_as(f64p),
+                                value_kind))
+
     def info(self):
         order = C.c_int()
         dims = np.zeros(8, np.uint64)

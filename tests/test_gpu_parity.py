@@ -436,3 +436,30 @@ def test_production_mask_equals_pick_sets(ntc, orc, lens):
             want[orc.sample_row(n, cf, orc.fork(orc.fork(st, 1), p))] = True
             got = bits[int(off[p]) - e0: int(off[p + 1]) - e0]
             np.testing.assert_array_equal(got, want)
+
+
+def test_zipf_heavy_slices_vs_oracle(ntc, orc):
+    """Zipf(1.2) modes: slices far beyond the sampler's shared-memory budget
+    (heavy-slice grid path) and beyond the 16384-entry work item (split rows +
+    k_finalize).  Three free-running sweeps against the fp64 restatement."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [5000, 400, 60], 400_000, 8
+    ctx = P.Context(0)
+    ctx.synth(dims, nnz, 6, 0.5, 77, [1.2, 1.2, 0.0], 1)
+    ci, cv = ctx.canonical()
+    assert np.all((cv >= 1) & (cv <= 5)) and np.all(cv == np.round(cv))
+    cv64 = cv.astype(np.float64)
+    views = [orc.build_view(dims, ci, cv64, m) for m in range(3)]
+    longest = max(int(np.diff(v[0].astype(np.int64)).max()) for v in views)
+    assert longest > 16384, longest  # > u32 smem cap (14336) and > one work item
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 7)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    for k in range(3):
+        ctx.sweep_async(k, P.NmcConfig(c=0.5), 7)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None, O.nmc_cfg(c=0.5, threads=8),
+                             orc.sweep_state(7, k, m)) for m in range(3))
+        assert acc == oacc
+        for m in range(3):
+            assert rel(ctx.get_factor(m)[0], F[m]) <= TOL, (k, m)
