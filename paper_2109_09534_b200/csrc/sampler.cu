@@ -388,12 +388,12 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
   a.mask = mask;
   a.counters = ctx->counters;
   a.direct = direct;
+  // 16-bit table (flag bit 15): slices up to 28672 entries (56 KB per warp)
+  // in shared memory; longer slices take the grid-wide heavy path.
   const uint64_t maxn = v.max_slice;
-  const bool small = maxn <= 32767;
-  const uint64_t esz = small ? 2 : 4;
-  uint64_t cap = maxn;
-  const uint64_t budget = 56 * 1024;
-  if (cap * esz > budget) cap = budget / esz;
+  const bool small = true;
+  const uint64_t esz = 2;
+  uint64_t cap = std::min<uint64_t>(maxn, v.light_cap ? v.light_cap : 28672);
   if (cap < 32) cap = 32;
   a.cap = cap;
   a.warp_bytes = static_cast<uint32_t>((cap * esz + 15) / 16 * 16);

@@ -301,8 +301,24 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
                               cudaMemcpyDeviceToHost, st));
     NTCB_CUDA(cudaStreamSynchronize(st));
     uint64_t mx = 0;
-    for (uint64_t p = 0; p < v.rows; ++p) mx = std::max(mx, v.h_off[p + 1] - v.h_off[p]);
+    std::vector<uint64_t> lens;
+    lens.reserve(v.rows);
+    for (uint64_t p = 0; p < v.rows; ++p) {
+      const uint64_t n = v.h_off[p + 1] - v.h_off[p];
+      mx = std::max(mx, n);
+      if (n > 1) lens.push_back(n);
+    }
     v.max_slice = mx;
+    // Sampler shared-memory cap: twice the 99th percentile slice (>= 2048, <= 28672
+    // entries, 2 bytes each); only the longer tail goes to the grid path, so a
+    // few Zipf-heavy slices do not force every warp to reserve 56 KB.
+    uint64_t cap = std::min<uint64_t>(mx, 28672);
+    if (lens.size() > 100) {
+      const size_t q = lens.size() - 1 - lens.size() / 100;
+      std::nth_element(lens.begin(), lens.begin() + q, lens.end());
+      cap = std::min<uint64_t>(cap, std::max<uint64_t>(2 * lens[q], 2048));
+    }
+    v.light_cap = (cap + 255) / 256 * 256;
   }
   ctx->mask_words = nnz / 32 + 2;
   for (int m = 0; m < order; ++m)
@@ -314,7 +330,7 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
   // Per-entry Fisher-Yates scratch for slices beyond the sampler's smem budget.
   uint64_t big = 0;
   for (int m = 0; m < order; ++m) big = std::max(big, ctx->views[m].max_slice);
-  if (big > 4096) {
+  if (big > 2048) {
     ctx->perm_scratch_n = nnz;
     NTCB_CUDA(cudaMalloc(&ctx->perm_scratch, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)));
   }
