@@ -98,13 +98,17 @@ class ShardedSweep:
             torch.cuda.set_stream(st)
         ctx.set_stream(st.cuda_stream)
 
-    def sweep(self, k: int, seed: int) -> None:
+    def sweep_mode(self, k: int, m: int, seed: int) -> None:
+        """This rank's rows of the mode-m update of sweep k, then the exchange."""
         from .ntc import sweep_stream
+        r0, r1 = self.bounds[m][self.rank]
+        self.ctx.s_nmc_rows_async(m, r0, r1, self.cfg, sweep_stream(seed, k, m).state)
+        if self.world > 1:
+            allgather_rows(self.A[m], self.bounds[m], self.rank, self.group)
+
+    def sweep(self, k: int, seed: int) -> None:
         for m in range(len(self.dims)):
-            r0, r1 = self.bounds[m][self.rank]
-            self.ctx.s_nmc_rows_async(m, r0, r1, self.cfg, sweep_stream(seed, k, m).state)
-            if self.world > 1:
-                allgather_rows(self.A[m], self.bounds[m], self.rank, self.group)
+            self.sweep_mode(k, m, seed)
 
     def local_sampled(self, m: int) -> int:
         r0, r1 = self.bounds[m][self.rank]
