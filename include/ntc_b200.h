@@ -126,6 +126,21 @@ int ntcb_view_export_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint6
 /* Canonical (lexicographic) COO, SparseTensor::indices()/values(). */
 int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values);
 
+/* ---- .tns files (tns_io.cpp:41-142), parallel host parser --------------
+ * Same syntax and diagnostics as read_tns ("path:line: message",
+ * std::runtime_error -> NTCB_ERUNTIME).  ntcb_tns_parse allocates *indices
+ * (nnz*order, 0-based) and *values with malloc (release with ntcb_free);
+ * host only, no device needed; its message is in ntcb_tns_last_error().
+ * ntcb_tensor_read_tns parses and loads (validation, canonical order and
+ * views on the device); ntcb_tns_write writes "# dims:" + 1-based %.17g. */
+int ntcb_tns_parse(const char* path, int* order, uint64_t* dims, uint64_t* nnz,
+                   uint32_t** indices, double** values);
+const char* ntcb_tns_last_error(void);
+void ntcb_free(void* p);
+int ntcb_tns_write(const char* path, int order, const uint64_t* dims, uint64_t nnz,
+                   const uint32_t* indices, const double* values);
+int ntcb_tensor_read_tns(ntcb_context* ctx, const char* path);
+
 /* ---- factors (FactorSet, factor_set.hpp:12-35) ------------------------- */
 /* factors/momentum: order pointers to host row-major double dims[m] x rank;
  * momentum may be NULL (= factors).  Factors must be nonnegative. */

@@ -287,8 +287,30 @@ def ref_lib():
                                    _f64p, _f64p]
         L.ref_row_terms.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _u32p, C.c_uint64, _f64p,
                                     C.c_double, _f64p, _f64p, _f64p, _f64p]
+        L.ref_read_tns.restype = C.c_void_p
+        L.ref_read_tns.argtypes = [C.c_char_p]
+        L.ref_order.restype = C.c_int
+        L.ref_order.argtypes = [C.c_void_p]
+        L.ref_dims.argtypes = [C.c_void_p, _u64p]
+        L.ref_write_tns.argtypes = [C.c_void_p, C.c_char_p]
         _REF = L
     return _REF
+
+
+def ref_read_tns(path):
+    """The reference's read_tns: (dims, canonical idx, vals) or raises with its message."""
+    L = ref_lib()
+    h = L.ref_read_tns(path.encode())
+    if not h:
+        raise RuntimeError(L.ref_last_error().decode())
+    p = RefProblem.__new__(RefProblem)
+    p.h = C.c_void_p(h)
+    p.rank = None
+    N = L.ref_order(p.h)
+    d = np.zeros(N, np.uint64)
+    L.ref_dims(p.h, _ptr(d, _u64p))
+    p.dims = d
+    return p
 
 
 def _ref_check(rc):

@@ -31,6 +31,7 @@
 #include "ntc/nmc.hpp"
 #include "ntc/rng.hpp"
 #include "ntc/sparse_tensor.hpp"
+#include "ntc/tns_io.hpp"
 
 namespace {
 
@@ -367,6 +368,27 @@ int ref_ao_ntc(void* h, const ref_ao_cfg* cfg, const double* init, double* out,
       hist[5 * i + 4] = static_cast<double>(rec.entries_accessed);
     }
   });
+}
+
+// read_tns (tns_io.cpp:41-125): a problem handle, or NULL with the error text.
+void* ref_read_tns(const char* path) {
+  Problem* out = nullptr;
+  int rc = guarded([&] {
+    auto p = std::make_unique<Problem>();
+    p->tensor.emplace(ntc::read_tns(path));
+    p->dims = p->tensor->dims();
+    p->views = ntc::build_mode_views(*p->tensor);
+    out = p.release();
+  });
+  return rc == 0 ? out : nullptr;
+}
+int ref_order(void* h) { return static_cast<int>(static_cast<Problem*>(h)->dims.size()); }
+void ref_dims(void* h, std::uint64_t* d) {
+  auto* p = static_cast<Problem*>(h);
+  for (std::size_t m = 0; m < p->dims.size(); ++m) d[m] = p->dims[m];
+}
+int ref_write_tns(void* h, const char* path) {
+  return guarded([&] { ntc::write_tns(*static_cast<Problem*>(h)->tensor, path); });
 }
 
 // ---- per-row operators ----------------------------------------------------

@@ -84,6 +84,12 @@ SIGNATURES = {
     "ntcb_view_export_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, u64p, u32p,
                                         f32p]),
     "ntcb_tensor_export": (C.c_int, [C.c_void_p, u32p, f32p]),
+    "ntcb_tns_parse": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), u64p, u64p, C.POINTER(u32p),
+                                 C.POINTER(f64p)]),
+    "ntcb_tns_last_error": (C.c_char_p, []),
+    "ntcb_free": (None, [C.c_void_p]),
+    "ntcb_tns_write": (C.c_int, [C.c_char_p, C.c_int, u64p, C.c_uint64, u32p, f64p]),
+    "ntcb_tensor_read_tns": (C.c_int, [C.c_void_p, C.c_char_p]),
     "ntcb_factors_init": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(f64p), C.POINTER(f64p)]),
     "ntcb_factors_random": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64]),
     "ntcb_factor_set": (C.c_int, [C.c_void_p, C.c_int, f64p, f64p]),

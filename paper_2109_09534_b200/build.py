@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libntcb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["capi.cu", "tensor.cu", "sampler.cu", "update.cu", "metrics.cu", "synth.cu"]
+SOURCES = ["capi.cu", "tensor.cu", "sampler.cu", "update.cu", "metrics.cu", "synth.cu", "tns.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -34,7 +34,7 @@ def _headers():
 
 
 def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     srcp = os.path.join(CSRC, src)
     newest = max(os.path.getmtime(p) for p in [srcp] + _headers())
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest:

@@ -384,6 +384,30 @@ int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
   API_CATCH
 }
 
+int ntcb_tensor_read_tns(ntcb_context* ctx, const char* path) {
+  API_TRY
+  need_ctx(ctx);
+  int order = 0;
+  uint64_t dims[NTCB_MAX_ORDER] = {};
+  uint64_t nnz = 0;
+  uint32_t* idx = nullptr;
+  double* val = nullptr;
+  const int rc = ntcb_tns_parse(path, &order, dims, &nnz, &idx, &val);
+  if (rc) fail(rc, ntcb_tns_last_error());
+  struct Free {
+    void* a;
+    void* b;
+    ~Free() {
+      ntcb_free(a);
+      ntcb_free(b);
+    }
+  } fr{idx, val};
+  free_factors(ctx);
+  load_tensor_f64(ctx, order, dims, nnz, idx, val);
+  g_host[ctx].bs_cache.clear();
+  API_CATCH
+}
+
 int ntcb_tensor_info(ntcb_context* ctx, int* order, uint64_t* dims, uint64_t* nnz) {
   API_TRY
   need_ctx(ctx);

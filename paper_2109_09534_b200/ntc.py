@@ -461,6 +461,47 @@ class SparseTensor:
         return float(np.sqrt(np.sum(v * v)))
 
 
+def parse_tns(path: str):
+    """Parallel host parse of a .tns file (ntcb_tns_parse; read_tns syntax and
+    diagnostics, tns_io.cpp:41-125): returns (dims, indices (nnz, N) 0-based,
+    values float64) in file order."""
+    L = _lib.load()
+    order = C.c_int()
+    dims = np.zeros(8, np.uint64)
+    nnz = C.c_uint64()
+    ip, vp = u32p(), f64p()
+    rc = L.ntcb_tns_parse(path.encode(), C.byref(order), dims.ctypes.data_as(u64p), C.byref(nnz),
+                          C.byref(ip), C.byref(vp))
+    if rc:
+        raise _lib._EXC.get(rc, NtcRuntimeError)(L.ntcb_tns_last_error().decode())
+    try:
+        N, n = order.value, nnz.value
+        idx = np.ctypeslib.as_array(ip, shape=(max(n * N, 1),))[: n * N].reshape(n, N).copy()
+        vals = np.ctypeslib.as_array(vp, shape=(max(n, 1),))[:n].copy()
+    finally:
+        L.ntcb_free(C.cast(ip, C.c_void_p))
+        L.ntcb_free(C.cast(vp, C.c_void_p))
+    return [int(d) for d in dims[:N]], idx, vals
+
+
+def read_tns(path: str, device: int = 0) -> "SparseTensor":
+    """ntc::read_tns (tns_io.cpp:41-125): parse in parallel, then build the
+    canonical tensor and mode views on the device."""
+    dims, idx, vals = parse_tns(path)
+    return SparseTensor(dims, idx, vals, device)
+
+
+def write_tns(t: "SparseTensor", path: str) -> None:
+    """ntc::write_tns (tns_io.cpp:127-142)."""
+    L = _lib.load()
+    idx, vals = t.ctx.canonical()
+    dims = np.ascontiguousarray(t.dims(), np.uint64)
+    idx = np.ascontiguousarray(idx, np.uint32)
+    v64 = np.ascontiguousarray(vals, np.float64)
+    check(L.ntcb_tns_write(path.encode(), len(dims), dims.ctypes.data_as(u64p), len(v64),
+                           idx.ctypes.data_as(u32p), v64.ctypes.data_as(f64p)))
+
+
 @dataclass
 class FactorSet:
     rank: int = 0

@@ -463,3 +463,27 @@ def test_zipf_heavy_slices_vs_oracle(ntc, orc):
         assert acc == oacc
         for m in range(3):
             assert rel(ctx.get_factor(m)[0], F[m]) <= TOL, (k, m)
+
+
+def test_read_write_tns_device(ntc, tmp_path, golden):
+    """read_tns -> device tensor (views as the reference's) -> write_tns -> read_tns."""
+    from paper_2109_09534_b200.ntc import read_tns, write_tns
+    dims = [int(d) for d in golden["t1_dims"]]
+    lines = [f"# dims: {' '.join(map(str, dims))}"]
+    for (a, b, c), v in zip(golden["t1_idx"].tolist(), golden["t1_vals"].tolist()):
+        lines.append(f"{a + 1} {b + 1} {c + 1} {v!r}")
+    path = tmp_path / "t1.tns"
+    path.write_text("\n".join(lines) + "\n")
+    t = read_tns(str(path))
+    for m in range(3):
+        off, oth, val = t.view(m)
+        np.testing.assert_array_equal(off, golden[f"t1_view{m}_off"])
+        np.testing.assert_array_equal(oth, golden[f"t1_view{m}_oth"])
+    out = tmp_path / "t1_out.tns"
+    write_tns(t, str(out))
+    t2 = read_tns(str(out))
+    np.testing.assert_array_equal(t2.indices(), t.indices())
+    np.testing.assert_array_equal(t2.values(), t.values())
+    c = ntc.Context(0)
+    c.L.ntcb_tensor_read_tns(c.h, str(path).encode())
+    np.testing.assert_array_equal(c.canonical()[0], golden["t1_canon_idx"])
