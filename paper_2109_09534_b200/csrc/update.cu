@@ -6,18 +6,23 @@
 // k_finalize reduces them in a fixed order -- deterministic, and a heavy row
 // no longer serialises on one warp).  ONE WARP per item, no block barriers:
 //
-//   stream  32 consecutive entries per step (coalesced SoA loads), keep the
+//   stream  128 consecutive entries per step (cp.async 128-bit loads of the
+//           SoA record arrays and the mask, double-buffered), keep the
 //           sampled ones (mask bit, or all at c >= 1), compact them with a
-//           ballot into a 64-slot staging ring in shared memory;
-//   gather  per 32 staged picks, lane i forms k = Hadamard product of the
-//           other factors' rows of pick i (kr_row, factor_set.cpp:42-64,
-//           float4 loads), s = y.k - x, accumulates g += s k in registers
-//           (= w + z of nmc.cpp:84-93) and writes k to a warp-private tile;
-//   Gram    each lane owns a 4x4 block of the R x R upper triangle and a
-//           pick group; 2 LDS.128 + 16 FFMA per pick (nmc.cpp:95-96).
+//           warp scan into a 256-slot staging ring in shared memory;
+//   gather  groups of 32/L picks, L = ld/4: lane (pick, s) loads feature
+//           block s of the pick's row in every other factor (a pick's L
+//           lanes read one contiguous row) and forms the Khatri-Rao block
+//           (kr_row, factor_set.cpp:42-64); the next group's loads are in
+//           flight while this group computes;
+//   Gram    lane role s owns block pairs (s, s+d), d <= L/2, with partner
+//           blocks fetched by shuffle -- every block pair of the upper
+//           triangle exactly once, operands in registers (nmc.cpp:95-96);
+//           w_s += x k_s on the side.
 //
 // Finalisation per row (warp, fp64): H = lambda I + sum k k^T (mirrored),
-// grad = sum s k + lambda y, finiteness checks (nmc.cpp:247-251, 145-146),
+// grad = H y - w + lambda y (= w + z + lambda y of nmc.cpp:84-105),
+// finiteness checks (nmc.cpp:247-251, 145-146),
 // power method from the normalised all-ones vector (nmc.cpp:140-172),
 // L = 1.01 rq (nmc.cpp:253-254), projected step + Nesterov momentum
 // (nmc.cpp:174-197).  fp32 accumulation; sums are taken in slice order over
@@ -128,9 +133,18 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
   const int HS = R | 1;
   const int ld = LD4 * 4;
   const double lam = a.lambda;
+  // On entry gd holds w = sum_e x_e k_e.  grad = sum_e (y.k_e - x_e) k_e + lambda y
+  // = H y - w + lambda y with H = sum k k^T (nmc.cpp:84-105).  Forming it here
+  // in fp64 instead of per pick is exact in real arithmetic; the fp32 error of
+  // the sums is relative to |H y| ~ L |y|, and the step divides by L, so the
+  // update error stays ~1e-6 |y| (tests/test_gpu_parity.py, TOL = 1e-4).
   bool bad = false;
+  const float* yrow = a.Y + p * ld;
   for (int r = lane; r < R; r += 32) {
-    gd[r] += lam * static_cast<double>(a.Y[p * ld + r]);
+    const float* hr = Hf + r * HS;
+    double hy = 0.0;
+    for (int q = 0; q < R; ++q) hy += static_cast<double>(hr[q]) * static_cast<double>(__ldg(yrow + q));
+    gd[r] = hy - gd[r] + lam * static_cast<double>(yrow[r]);
     bad |= !isfinite(gd[r]);
   }
   __syncwarp();
@@ -240,8 +254,6 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
     const WorkItem w = a.items[it];
     const uint64_t p = w.row;
 
-    // y block s (gradient taken at Y, nmc.cpp:244-246)
-    const float4 ys = reinterpret_cast<const float4*>(a.Y + p * ld)[s];
     float acc[ND][16];
 #pragma unroll
     for (int d = 0; d < ND; ++d)
@@ -253,9 +265,8 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
 
     // One group of np <= GP picks: lane (pk, s) gathers feature block s of
     // pick pk from every other factor's row (the L lanes of a pick read one
-    // contiguous row), forms the Khatri-Rao block, the residual s = y.k - x
-    // (segment sum over the pick's L lanes), the gradient block, and the
-    // Gram blocks (s, s+d) with partner blocks fetched by shuffle.
+    // contiguous row), forms the Khatri-Rao block, accumulates w_s += x k_s
+    // and the Gram blocks (s, s+d) with partner blocks fetched by shuffle.
     // A group's gather (load_group) is issued one group ahead of its
     // arithmetic (compute_group) so the L2 latency of the factor rows hides
     // behind the previous group's Gram update.
@@ -292,19 +303,13 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
           kb.w *= g.f[m].w;
         }
       }
-      float dp = ys.x * kb.x;
-      dp = fmaf(ys.y, kb.y, dp);
-      dp = fmaf(ys.z, kb.z, dp);
-      dp = fmaf(ys.w, kb.w, dp);
-      float dot = 0.f;
+      // w += x k  (the gradient is formed as H y - w at the row end)
       const int base = (lane_on ? pk : 0) * L;
-#pragma unroll
-      for (int t = 0; t < L; ++t) dot += __shfl_sync(0xffffffffu, dp, base + t);
-      const float sres = on ? dot - g.x : 0.f;
-      gl.x = fmaf(sres, kb.x, gl.x);
-      gl.y = fmaf(sres, kb.y, gl.y);
-      gl.z = fmaf(sres, kb.z, gl.z);
-      gl.w = fmaf(sres, kb.w, gl.w);
+      const float xw = on ? g.x : 0.f;
+      gl.x = fmaf(xw, kb.x, gl.x);
+      gl.y = fmaf(xw, kb.y, gl.y);
+      gl.z = fmaf(xw, kb.z, gl.z);
+      gl.w = fmaf(xw, kb.w, gl.w);
       const float ka[4] = {kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
