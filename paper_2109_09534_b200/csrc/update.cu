@@ -272,7 +272,6 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
     // behind the previous group's Gram update.
     struct Raw {
       float4 f[NO];
-      float x;
     };
     auto load_group = [&](int at, int np) {
       Raw g;
@@ -280,9 +279,7 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       const int sidx = (at + pk) & (W::kStage - 1);
 #pragma unroll
       for (int m = 0; m < NO; ++m) g.f[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-      g.x = 0.f;
       if (on) {
-        g.x = st_x[sidx];
 #pragma unroll
         for (int m = 0; m < NO; ++m)
           if (m < no)
@@ -291,8 +288,9 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       return g;
     };
-    auto compute_group = [&](const Raw& g, int np) {
+    auto compute_group = [&](const Raw& g, int np, int at) {
       const bool on = lane_on && pk < np;
+      const float gx = on ? st_x[(at + pk) & (W::kStage - 1)] : 0.f;
       float4 kb = g.f[0];
 #pragma unroll
       for (int m = 1; m < NO; ++m) {
@@ -305,7 +303,7 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       // w += x k  (the gradient is formed as H y - w at the row end)
       const int base = (lane_on ? pk : 0) * L;
-      const float xw = on ? g.x : 0.f;
+      const float xw = gx;
       gl.x = fmaf(xw, kb.x, gl.x);
       gl.y = fmaf(xw, kb.y, gl.y);
       gl.z = fmaf(xw, kb.z, gl.z);
@@ -347,20 +345,39 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       const int rem = cnt - ng * GP;
       const int total_g = ng + ((flush && rem > 0) ? 1 : 0);
       if (total_g == 0) return;
-      int at = head;
-      Raw ra = load_group(at, ng > 0 ? GP : rem);
-      for (int g = 0; g < total_g; g += 2) {
-        const int npa = g < ng ? GP : rem;
-        Raw rb;
-        const bool hb = g + 1 < total_g;
-        const int npb = g + 1 < ng ? GP : rem;
-        if (hb) rb = load_group((at + npa) & (W::kStage - 1), npb);
-        compute_group(ra, npa);
-        at = (at + npa) & (W::kStage - 1);
-        if (hb) {
-          if (g + 2 < total_g) ra = load_group((at + npb) & (W::kStage - 1), g + 2 < ng ? GP : rem);
-          compute_group(rb, npb);
-          at = (at + npb) & (W::kStage - 1);
+      auto npof = [&](int g) { return g < ng ? GP : rem; };
+      // three-way rotation: the loads of groups g+1 and g+2 are in flight
+      // while group g computes
+      int al = head, ac = head;
+      Raw r0, r1, r2;
+      r0 = load_group(al, npof(0));
+      al = (al + npof(0)) & (W::kStage - 1);
+      if (1 < total_g) {
+        r1 = load_group(al, npof(1));
+        al = (al + npof(1)) & (W::kStage - 1);
+      }
+      for (int g = 0; g < total_g; g += 3) {
+        if (g + 2 < total_g) {
+          r2 = load_group(al, npof(g + 2));
+          al = (al + npof(g + 2)) & (W::kStage - 1);
+        }
+        compute_group(r0, npof(g), ac);
+        ac = (ac + npof(g)) & (W::kStage - 1);
+        if (g + 1 < total_g) {
+          if (g + 3 < total_g) {
+            r0 = load_group(al, npof(g + 3));
+            al = (al + npof(g + 3)) & (W::kStage - 1);
+          }
+          compute_group(r1, npof(g + 1), ac);
+          ac = (ac + npof(g + 1)) & (W::kStage - 1);
+          if (g + 2 < total_g) {
+            if (g + 4 < total_g) {
+              r1 = load_group(al, npof(g + 4));
+              al = (al + npof(g + 4)) & (W::kStage - 1);
+            }
+            compute_group(r2, npof(g + 2), ac);
+            ac = (ac + npof(g + 2)) & (W::kStage - 1);
+          }
         }
       }
       const int used = ng * GP + ((flush && rem > 0) ? rem : 0);
