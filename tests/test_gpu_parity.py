@@ -487,3 +487,37 @@ def test_read_write_tns_device(ntc, tmp_path, golden):
     c = ntc.Context(0)
     c.L.ntcb_tensor_read_tns(c.h, str(path).encode())
     np.testing.assert_array_equal(c.canonical()[0], golden["t1_canon_idx"])
+
+
+@pytest.mark.parametrize("order,R", [(2, 1), (2, 7), (3, 1), (3, 4), (3, 13), (3, 32), (3, 41),
+                                     (3, 64), (4, 16), (5, 6), (6, 9)])
+def test_ranks_and_orders_vs_oracle(ntc, orc, order, R):
+    """Every kernel instantiation class: L = ceil(R/4) from 1 to 16 (incl. the
+    register-spilling large-R ones), orders 2..6 (the generic-order path);
+    two sweeps against the fp64 restatement."""
+    import paper_2109_09534_b200 as P
+    rng = np.random.default_rng(order * 100 + R)
+    dims = [int(x) for x in rng.integers(6, 40, size=order)]
+    cells = int(np.prod(dims))
+    nnz = min(cells // 2, 20000)
+    lin = rng.choice(cells, nnz, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), 1).astype(np.uint32)
+    vals = (rng.random(nnz) * 2).astype(np.float32)
+    ctx = P.Context(0)
+    ctx.load(dims, idx, vals)
+    ci, cv = orc.canonicalize(dims, idx, vals.astype(np.float64))
+    views = [orc.build_view(dims, ci, cv, m) for m in range(order)]
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 3)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    for k in range(2):
+        ctx.sweep_async(k, P.NmcConfig(c=0.6, max_inner=2, lambda_=1e-2), 9)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None,
+                             O.nmc_cfg(c=0.6, max_inner=2, lambda_=1e-2, threads=8),
+                             orc.sweep_state(9, k, m)) for m in range(order))
+        assert acc == oacc
+        for m in range(order):
+            a, y = ctx.get_factor(m)
+            assert rel(a, F[m]) <= TOL, (k, m, rel(a, F[m]))
+            assert rel(y, M[m]) <= TOL, (k, m, rel(y, M[m]))
