@@ -273,24 +273,37 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
     struct Raw {
       float4 f[NO];
     };
-    auto load_group = [&](int at, int np) {
+    // Full groups (GP picks): lanes beyond GP*L load factor row 0 (valid,
+    // discarded by the slot reduction), so no predicates or zero fills.
+    auto load_full = [&](int at) {
+      Raw g;
+      const int sidx = (at + pk) & (W::kStage - 1);
+#pragma unroll
+      for (int m = 0; m < NO; ++m)
+        if (m < no) {
+          const uint32_t row = lane_on ? st_o[m * W::kStage + sidx] : 0u;
+          g.f[m] = __ldg(reinterpret_cast<const float4*>(a.U[m] + static_cast<uint64_t>(row) * ld) + s);
+        }
+      return g;
+    };
+    // The partial last group of an item: lanes of absent picks contribute 0.
+    auto load_part = [&](int at, int np) {
       Raw g;
       const bool on = lane_on && pk < np;
       const int sidx = (at + pk) & (W::kStage - 1);
 #pragma unroll
-      for (int m = 0; m < NO; ++m) g.f[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (on) {
-#pragma unroll
-        for (int m = 0; m < NO; ++m)
-          if (m < no)
-            g.f[m] = __ldg(reinterpret_cast<const float4*>(
-                               a.U[m] + static_cast<uint64_t>(st_o[m * W::kStage + sidx]) * ld) + s);
-      }
+      for (int m = 0; m < NO; ++m)
+        if (m < no) {
+          const uint32_t row = on ? st_o[m * W::kStage + sidx] : 0u;
+          g.f[m] = __ldg(reinterpret_cast<const float4*>(a.U[m] + static_cast<uint64_t>(row) * ld) + s);
+          if (!on) g.f[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       return g;
     };
-    auto compute_group = [&](const Raw& g, int np, int at) {
-      const bool on = lane_on && pk < np;
-      const float gx = on ? st_x[(at + pk) & (W::kStage - 1)] : 0.f;
+    auto compute_group = [&](const Raw& g, int at, int np) {
+      // lanes of absent picks in a partial group must add exact zeros (stale
+      // ring slots may hold anything); lanes beyond GP*L are never reduced
+      const float gx = pk < np ? st_x[(at + pk) & (W::kStage - 1)] : 0.f;
       float4 kb = g.f[0];
 #pragma unroll
       for (int m = 1; m < NO; ++m) {
@@ -303,11 +316,10 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       // w += x k  (the gradient is formed as H y - w at the row end)
       const int base = (lane_on ? pk : 0) * L;
-      const float xw = gx;
-      gl.x = fmaf(xw, kb.x, gl.x);
-      gl.y = fmaf(xw, kb.y, gl.y);
-      gl.z = fmaf(xw, kb.z, gl.z);
-      gl.w = fmaf(xw, kb.w, gl.w);
+      gl.x = fmaf(gx, kb.x, gl.x);
+      gl.y = fmaf(gx, kb.y, gl.y);
+      gl.z = fmaf(gx, kb.z, gl.z);
+      gl.w = fmaf(gx, kb.w, gl.w);
       const float ka[4] = {kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
@@ -338,60 +350,58 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
         }
       }
     };
-    // all full groups currently staged, software-pipelined one group deep
-    // (ping-pong registers: no copies that would wait on in-flight loads)
-    auto drain = [&](bool flush) {
+    // All staged full groups, three-way rotation: the gathers of groups g+1
+    // and g+2 are in flight while group g computes (no register copies that
+    // would wait on in-flight loads).
+    auto drain_full = [&]() {
       const int ng = cnt / GP;
-      const int rem = cnt - ng * GP;
-      const int total_g = ng + ((flush && rem > 0) ? 1 : 0);
-      if (total_g == 0) return;
-      auto npof = [&](int g) { return g < ng ? GP : rem; };
-      // three-way rotation: the loads of groups g+1 and g+2 are in flight
-      // while group g computes
+      if (ng == 0) return;
       int al = head, ac = head;
       Raw r0, r1, r2;
-      r0 = load_group(al, npof(0));
-      al = (al + npof(0)) & (W::kStage - 1);
-      if (1 < total_g) {
-        r1 = load_group(al, npof(1));
-        al = (al + npof(1)) & (W::kStage - 1);
+      r0 = load_full(al);
+      al = (al + GP) & (W::kStage - 1);
+      if (1 < ng) {
+        r1 = load_full(al);
+        al = (al + GP) & (W::kStage - 1);
       }
-      for (int g = 0; g < total_g; g += 3) {
-        if (g + 2 < total_g) {
-          r2 = load_group(al, npof(g + 2));
-          al = (al + npof(g + 2)) & (W::kStage - 1);
+      for (int g = 0; g < ng; g += 3) {
+        if (g + 2 < ng) {
+          r2 = load_full(al);
+          al = (al + GP) & (W::kStage - 1);
         }
-        compute_group(r0, npof(g), ac);
-        ac = (ac + npof(g)) & (W::kStage - 1);
-        if (g + 1 < total_g) {
-          if (g + 3 < total_g) {
-            r0 = load_group(al, npof(g + 3));
-            al = (al + npof(g + 3)) & (W::kStage - 1);
+        compute_group(r0, ac, GP);
+        ac = (ac + GP) & (W::kStage - 1);
+        if (g + 1 < ng) {
+          if (g + 3 < ng) {
+            r0 = load_full(al);
+            al = (al + GP) & (W::kStage - 1);
           }
-          compute_group(r1, npof(g + 1), ac);
-          ac = (ac + npof(g + 1)) & (W::kStage - 1);
-          if (g + 2 < total_g) {
-            if (g + 4 < total_g) {
-              r1 = load_group(al, npof(g + 4));
-              al = (al + npof(g + 4)) & (W::kStage - 1);
+          compute_group(r1, ac, GP);
+          ac = (ac + GP) & (W::kStage - 1);
+          if (g + 2 < ng) {
+            if (g + 4 < ng) {
+              r1 = load_full(al);
+              al = (al + GP) & (W::kStage - 1);
             }
-            compute_group(r2, npof(g + 2), ac);
-            ac = (ac + npof(g + 2)) & (W::kStage - 1);
+            compute_group(r2, ac, GP);
+            ac = (ac + GP) & (W::kStage - 1);
           }
         }
       }
-      const int used = ng * GP + ((flush && rem > 0) ? rem : 0);
-      head = (head + used) & (W::kStage - 1);
-      cnt -= used;
+      head = (head + ng * GP) & (W::kStage - 1);
+      cnt -= ng * GP;
     };
 
-    // ---- stream the item in batches of 128 entries (4 per lane, 128-bit
-    // loads issued independently of the mask), prefetching the next batch
-    // while the current one is compacted and processed ----
+    // ---- stream the item in batches of 128 entries (4 per lane; cp.async
+    // 128-bit loads of the SoA records and the mask word, double-buffered,
+    // issued independently of the mask) ----
     const uint64_t tb = w.e0 & ~uint64_t(3);  // 16-byte aligned start
-    auto fetch_async = [&](uint64_t t, int buf) {
-      const uint64_t e = t + 4 * lane;
-      if (e < w.e1) {
+    const int lo = static_cast<int>(w.e0 - tb);          // item start, relative to tb
+    const int hi = static_cast<int>(w.e1 - tb);          // item end, relative to tb
+    auto fetch_async = [&](int t, int buf) {
+      const int r = t + 4 * lane;
+      if (r < hi) {
+        const uint64_t e = tb + static_cast<uint64_t>(r);
 #pragma unroll
         for (int m = 0; m < NO + 1; ++m) {
           if (m < no || m == NO) {
@@ -409,10 +419,11 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       asm volatile("cp.async.commit_group;\n" ::);
     };
-    fetch_async(tb, 0);
+    const uint32_t sh0 = static_cast<uint32_t>(tb & 31u);  // bit of rel 0 in its mask word
+    fetch_async(0, 0);
     int buf = 0;
-    for (uint64_t t0 = tb; t0 < w.e1; t0 += 128, buf ^= 1) {
-      if (t0 + 128 < w.e1) {
+    for (int t0 = 0; t0 < hi; t0 += 128, buf ^= 1) {
+      if (t0 + 128 < hi) {
         fetch_async(t0 + 128, buf ^ 1);
         asm volatile("cp.async.wait_group 1;\n" ::);
       } else {
@@ -423,12 +434,11 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       for (int m = 0; m < NO; ++m)
         if (m < no) co[m] = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + m) * 128)[lane];
       const uint4 cv = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + no) * 128)[lane];
-      const uint32_t cm = full ? 0xffffffffu : rmsk[buf * 32 + lane];
-      const uint64_t e = t0 + 4 * lane;
-      uint32_t bits = full ? 0xfu : (cm >> (e & 31u)) & 0xfu;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (e + q < w.e0 || e + q >= w.e1) bits &= ~(1u << q);
+      const int r = t0 + 4 * lane;
+      uint32_t bits = full ? 0xfu : (rmsk[buf * 32 + lane] >> ((sh0 + static_cast<uint32_t>(r)) & 31u)) & 0xfu;
+      // clip to [lo, hi)
+      if (r < lo) bits &= 0xfu << (lo - r);
+      if (r + 4 > hi) bits &= hi - r > 0 ? (0xfu >> (4 - (hi - r))) : 0u;
       const int c4 = __popc(bits);
       int incl = c4;
 #pragma unroll
@@ -451,9 +461,14 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
       }
       cnt += total;
       __syncwarp();
-      drain(false);
+      drain_full();
     }
-    drain(true);
+    if (cnt > 0) {  // the item's last, partial group
+      const Raw rp = load_part(head, cnt);
+      compute_group(rp, head, cnt);
+      head = (head + cnt) & (W::kStage - 1);
+      cnt = 0;
+    }
 
     // ---- reduce over the GP pick slots (lanes with equal role s) ----------
 #pragma unroll 1
