@@ -208,7 +208,10 @@ def run_ours(args, cfgd, cid):
     torch.cuda.set_device(local)
     stream = torch.cuda.Stream()  # a real stream handle (the legacy default is NULL)
     torch.cuda.set_stream(stream)
-    if world > 1:
+    # NTCB_FORCE_SHARDED=1 (under torchrun) drives the multi-GPU code path --
+    # NCCL init, row shards, all-gather, sharded e2e -- even at one rank
+    distributed = world > 1 or os.environ.get("NTCB_FORCE_SHARDED") == "1"
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims, R = cfgd["dims"], cfgd["R"]
     order = len(dims)
@@ -217,7 +220,7 @@ def run_ours(args, cfgd, cid):
     generate(ctx, cfgd, cid)
     ctx.random_factors(R, SEED_SOLVER)
     cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
-    sharded = ShardedSweep(ctx, cfg, rank, world) if world > 1 else None
+    sharded = ShardedSweep(ctx, cfg, rank, world) if distributed else None
     offs = [ctx.view_offsets(m) for m in range(order)]
     full = sum(int(blocksizes(o, cfg.c).sum()) for o in offs)
     rows_processed = sum(int((blocksizes(o, cfg.c) > 0).sum()) for o in offs)
@@ -231,7 +234,7 @@ def run_ours(args, cfgd, cid):
     for k in range(args.warmup):
         step(k)
     ctx.collect()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -241,7 +244,7 @@ def run_ours(args, cfgd, cid):
         time.sleep(0.3)
     ctx.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record()
@@ -261,7 +264,7 @@ def run_ours(args, cfgd, cid):
         k += 1
         ctx.collect()
     clocks = clk.stop() if rank == 0 else None
-    if world > 1:
+    if distributed:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -285,7 +288,7 @@ def run_ours(args, cfgd, cid):
 
     # ---- end to end through the host-buffer C-ABI --------------------------------
     e2e = None
-    if world == 1:
+    if not distributed:
         Fh = [np.ascontiguousarray(ctx.get_factor(m)[0]) for m in range(order)]
         outs = [(np.zeros_like(f), np.zeros_like(f)) for f in Fh]
         ld = (R + 3) // 4 * 4
@@ -374,7 +377,7 @@ def run_ours(args, cfgd, cid):
             "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
