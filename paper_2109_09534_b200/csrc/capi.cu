@@ -282,9 +282,9 @@ int ntcb_create(int device, ntcb_context** out) {
     for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& mm : ctx->ev_consumed)
     for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  NTCB_CUDA(cudaMalloc(&ctx->counters, 4 * sizeof(unsigned long long)));
-  NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 4 * sizeof(unsigned long long)));
-  const unsigned long long init[4] = {0, ~0ull, 0, 0};
+  NTCB_CUDA(cudaMalloc(&ctx->counters, 8 * sizeof(unsigned long long)));
+  NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 8 * sizeof(unsigned long long)));
+  const unsigned long long init[8] = {0, ~0ull, 0, 0, 0, 0, 0, 0};
   NTCB_CUDA(cudaMemcpy(ctx->counters, init, sizeof init, cudaMemcpyHostToDevice));
   for (auto& e : ctx->prof.ev) NTCB_CUDA(cudaEventCreate(&e));
   g_host[ctx] = HostState{};

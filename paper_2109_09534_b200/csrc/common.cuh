@@ -123,7 +123,7 @@ struct ntcb_context {
   uint64_t perm_scratch_n = 0;
   int* heavy_flags = nullptr;  // per heavy slice: a draw may need Lemire rejection
   uint32_t heavy_flags_n = 0;
-  unsigned long long* counters = nullptr;  // [1] first error key, [2] work cursor
+  unsigned long long* counters = nullptr;  // [1] first error key, [2],[3] update cursors, [4],[5] sampler cursors
   unsigned long long* h_counters = nullptr;  // pinned mirror
   double* red = nullptr;  // metrics partials
   uint64_t red_n = 0;

@@ -372,44 +372,248 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Mid-length slices (kWarpCap < n <= cap): the same set formulation with a
+// whole CTA per slice, so a 10^4-entry slice is not one warp's serial
+// chain-walk.  T is u32 in shared memory (4n bytes); phase 1 is one shared
+// atomicMax per draw (order-free: the max is the last writer); the phases
+// are separated by __syncthreads.  Slices are taken from a host-built list
+// (longest first) through a device cursor, so CTAs stay busy to the end.
+// ---------------------------------------------------------------------------
+constexpr int kCtaThreads = 256;
+constexpr uint32_t kWarpCap = 1024;  // slices up to this length: warp per slice
+
+struct CtaArgs {
+  const uint64_t* off;
+  const uint32_t* rows;  // slice list (view rows), longest first
+  uint32_t n_rows;
+  double c;
+  uint64_t root;
+  uint32_t* mask;
+  unsigned long long* counters;  // [1] error key
+  unsigned long long* cursor;    // zeroed before the launch
+};
+
+__global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
+  constexpr uint32_t FLAG = 0x80000000u, VAL = 0x7fffffffu;
+  constexpr int NW = kCtaThreads / 32;
+  extern __shared__ __align__(16) uint32_t T[];
+  __shared__ unsigned long long s_item;
+  __shared__ int s_rej;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+  while (true) {
+    if (tid == 0) {
+      s_item = atomicAdd(a.cursor, 1ull);
+      s_rej = 0;
+    }
+    __syncthreads();
+    const unsigned long long item = s_item;
+    if (item >= a.n_rows) break;
+    const uint64_t p = a.rows[item];
+    const uint64_t beg = a.off[p];
+    const uint32_t n = static_cast<uint32_t>(a.off[p + 1] - beg);
+    const uint32_t b = static_cast<uint32_t>(blocksize_for(a.c, n));
+    const uint64_t state0 = fork64(a.root, p);
+    const uint32_t pw = (n + 3) / 4;
+    uint4* t4 = reinterpret_cast<uint4*>(T);
+    for (uint32_t w = tid; w < pw; w += kCtaThreads) t4[w] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    // ---- phase 1: T[r_j] = max(j + 1) over draws j with r_j != j ------------
+    {
+      bool rej = false;
+      uint64_t s = state0 + static_cast<uint64_t>(tid + 1) * kGolden;
+      for (uint32_t j = tid; j < b; j += kCtaThreads, s += kCtaThreads * kGolden) {
+        const uint32_t bound = n - j;
+        const uint64_t x = mix64(s);
+        const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
+        const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
+        rej |= static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound;
+        const uint32_t r = j + static_cast<uint32_t>(u >> 32);
+        if (r != j) atomicMax(&T[r], j + 1);
+      }
+      if (rej) s_rej = 1;
+    }
+    __syncthreads();
+    if (s_rej) {  // rare: a draw may need Lemire's rejection loop -- exact serial replay
+      for (uint32_t w = tid; w < pw; w += kCtaThreads) t4[w] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      if (tid == 0) {
+        uint64_t s = state0;
+        for (uint32_t j = 0; j < b; ++j) {
+          const uint64_t bd = n - j;
+          s += kGolden;
+          uint64_t xx = mix64(s);
+          uint64_t l2 = xx * bd, h2 = __umul64hi(xx, bd);
+          if (l2 < bd) {
+            const uint64_t th = (0 - bd) % bd;
+            while (l2 < th) {
+              s += kGolden;
+              xx = mix64(s);
+              l2 = xx * bd;
+              h2 = __umul64hi(xx, bd);
+            }
+          }
+          const uint32_t r = j + static_cast<uint32_t>(h2);
+          if (r != j) T[r] = j + 1;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- phase 2a: positions [b, n): picked iff targeted; flag unpicked roots
+    uint32_t* gm = a.mask + (beg >> 5);
+    const int off0 = static_cast<int>(beg & 31u);
+    const int kb0 = (static_cast<int>(b) + off0) >> 5;
+    const int kend = (static_cast<int>(n) + off0 - 1) >> 5;
+    for (int k = kb0 + wid; k <= kend; k += NW) {
+      const int t = 32 * k - off0 + lane;
+      const bool valid = t >= static_cast<int>(b) && t < static_cast<int>(n);
+      const uint32_t tv = valid ? (T[t] & VAL) : 0u;
+      if (tv) {
+        uint32_t v = tv - 1, nx;
+        while ((nx = T[v] & VAL) != 0u) v = nx - 1;
+        T[v] = FLAG;  // roots hold 0: the flag alone (concurrent walkers mask it off)
+      }
+      const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+      if (lane == 0) {
+        const bool whole = 32 * k - off0 >= static_cast<int>(b) && 32 * k - off0 + 32 <= static_cast<int>(n);
+        if (whole)
+          gm[k] = bits;
+        else if (bits)
+          atomicOr(&gm[k], bits);
+      }
+    }
+    __syncthreads();
+    // ---- phase 2b: values [0, b): picked unless flagged -----------------------
+    const int kbend = (static_cast<int>(b) + off0 - 1) >> 5;
+    for (int k = wid; k <= kbend; k += NW) {
+      const int t = 32 * k - off0 + lane;
+      const bool pick = t >= 0 && t < static_cast<int>(b) && !(T[t] & FLAG);
+      const uint32_t bits = __ballot_sync(kFull, pick);
+      if (lane == 0) {
+        const bool whole = 32 * k - off0 >= 0 && 32 * k - off0 + 32 <= static_cast<int>(b);
+        if (whole)
+          gm[k] = bits;
+        else if (bits)
+          atomicOr(&gm[k], bits);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Per (view, row range, cap): how many short slices, and the mid-slice list.
+struct SamplePlan {
+  uint64_t n_short = 0;
+  uint32_t* mid = nullptr;
+  uint32_t n_mid = 0;
+  uint32_t max_mid = 0;
+};
+static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, SamplePlan> g_splans;
+
+static const SamplePlan& sample_plan(const DeviceView& v, uint64_t r0, uint64_t r1, uint64_t cap) {
+  auto key = std::make_tuple(static_cast<const void*>(v.off), r0, r1, cap);
+  auto it = g_splans.find(key);
+  if (it != g_splans.end()) return it->second;
+  SamplePlan pl;
+  std::vector<std::pair<uint64_t, uint32_t>> mid;
+  for (uint64_t p = r0; p < r1; ++p) {
+    const uint64_t n = v.h_off[p + 1] - v.h_off[p];
+    if (n < 2) continue;  // b = floor(c n) = 0 for c < 1
+    if (n <= kWarpCap)
+      ++pl.n_short;
+    else if (n <= cap)
+      mid.emplace_back(n, static_cast<uint32_t>(p));
+  }
+  std::stable_sort(mid.begin(), mid.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  if (!mid.empty()) {
+    std::vector<uint32_t> rows(mid.size());
+    for (size_t i = 0; i < mid.size(); ++i) rows[i] = mid[i].second;
+    NTCB_CUDA(cudaMalloc(&pl.mid, sizeof(uint32_t) * rows.size()));
+    NTCB_CUDA(cudaMemcpy(pl.mid, rows.data(), sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice));
+    pl.n_mid = static_cast<uint32_t>(rows.size());
+    pl.max_mid = static_cast<uint32_t>(mid.front().first);
+  }
+  return g_splans.emplace(key, pl).first->second;
+}
+
+// Short slices on the warp kernel, mid slices on the CTA kernel; returns the
+// number of launches and the cap above which launch_sample_heavy takes over.
 int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
                       uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
                       uint64_t* heavy_cap) {
   const DeviceView& v = ctx->views[mode];
-  if (row_end <= row_begin) return 0;
+  if (heavy_cap) *heavy_cap = ~0ull;
+  if (row_end <= row_begin || c >= 1.0) return 0;
   if (v.max_slice >= (1ull << 31))
     fail(NTCB_EINVAL, "sampler: slices of 2^31 or more entries are not supported");
-  SampleArgs a{};
-  a.off = v.off;
-  a.row_begin = row_begin;
-  a.row_end = row_end;
-  a.c = c;
-  a.root = root;
-  a.mask = mask;
-  a.counters = ctx->counters;
-  a.direct = direct;
-  // 16-bit table (flag bit 15): slices up to 28672 entries (56 KB per warp)
-  // in shared memory; longer slices take the grid-wide heavy path.
-  const uint64_t maxn = v.max_slice;
-  const bool small = true;
-  const uint64_t esz = 2;
-  uint64_t cap = std::min<uint64_t>(maxn, v.light_cap ? v.light_cap : 28672);
-  if (cap < 32) cap = 32;
-  a.cap = cap;
-  a.warp_bytes = static_cast<uint32_t>((cap * esz + 15) / 16 * 16);
+  // shared-memory cap of the CTA kernel: u32 per entry, <= 48K entries
+  uint64_t cap = std::min<uint64_t>(v.max_slice, v.light_cap ? v.light_cap : 49152);
+  if (cap < kWarpCap) cap = kWarpCap;
   if (heavy_cap) *heavy_cap = cap;
-  const size_t smem = static_cast<size_t>(a.warp_bytes) * kSampleWarps;
-  int per_sm = 0;
-  auto kern = small ? k_sample_set<uint16_t> : k_sample_set<uint32_t>;
-  NTCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSampleWarps * 32, smem));
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t rows = row_end - row_begin;
-  uint64_t grid = (rows + kSampleWarps - 1) / kSampleWarps;
-  grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
-  kern<<<static_cast<unsigned>(grid), kSampleWarps * 32, smem, stream>>>(a);
-  NTCB_CUDA(cudaGetLastError());
-  return 1;
+  const SamplePlan& pl = sample_plan(v, row_begin, row_end, cap);
+  int launches = 0;
+  if (pl.n_short) {
+    SampleArgs a{};
+    a.off = v.off;
+    a.row_begin = row_begin;
+    a.row_end = row_end;
+    a.c = c;
+    a.root = root;
+    a.mask = mask;
+    a.counters = ctx->counters;
+    a.direct = direct;
+    a.cap = std::min<uint64_t>(v.max_slice, kWarpCap);
+    a.warp_bytes = static_cast<uint32_t>((a.cap * 2 + 15) / 16 * 16);
+    const size_t smem = static_cast<size_t>(a.warp_bytes) * kSampleWarps;
+    int per_sm = 0;
+    NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_set<uint16_t>,
+                                                            kSampleWarps * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (row_end - row_begin + kSampleWarps - 1) / kSampleWarps;
+    grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+    k_sample_set<uint16_t><<<static_cast<unsigned>(grid), kSampleWarps * 32, smem, stream>>>(a);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (pl.n_mid) {
+    if (direct) fail(NTCB_EINVAL, "sampler: direct streams are single-slice (warp kernel)");
+    CtaArgs a{};
+    a.off = v.off;
+    a.rows = pl.mid;
+    a.n_rows = pl.n_mid;
+    a.c = c;
+    a.root = root;
+    a.mask = mask;
+    a.counters = ctx->counters;
+    a.cursor = ctx->counters + (stream == ctx->side ? 4 : 5);
+    const size_t smem = (static_cast<size_t>(pl.max_mid) * 4 + 15) / 16 * 16;
+    NTCB_CUDA(cudaFuncSetAttribute(k_sample_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    int per_sm = 0;
+    NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_cta, kCtaThreads, smem));
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t grid = std::min<uint64_t>(pl.n_mid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+    NTCB_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), stream));
+    k_sample_cta<<<static_cast<unsigned>(grid), kCtaThreads, smem, stream>>>(a);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
+}
+
+void drop_sample_plans(ntcb_context* ctx) {
+  for (auto it = g_splans.begin(); it != g_splans.end();) {
+    bool mine = false;
+    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
+      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
+    if (mine) {
+      if (it->second.mid) cudaFree(it->second.mid);
+      it = g_splans.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -172,10 +172,12 @@ void radix_pairs(ntcb_context* ctx, KT* keys, KT* keys_alt, uint32_t* vals, uint
 
 void drop_plans(ntcb_context* ctx);
 void drop_heavy(ntcb_context* ctx);
+void drop_sample_plans(ntcb_context* ctx);
 
 void free_views(ntcb_context* ctx) {
   drop_plans(ctx);
   drop_heavy(ctx);
+  drop_sample_plans(ctx);
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
     DeviceView& v = ctx->views[m];
     if (v.off) cudaFree(v.off);
@@ -309,10 +311,10 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
       if (n > 1) lens.push_back(n);
     }
     v.max_slice = mx;
-    // Sampler shared-memory cap: twice the 99th percentile slice (>= 2048, <= 28672
-    // entries, 2 bytes each); only the longer tail goes to the grid path, so a
-    // few Zipf-heavy slices do not force every warp to reserve 56 KB.
-    uint64_t cap = std::min<uint64_t>(mx, 28672);
+    // Sampler shared-memory cap (CTA kernel, 4 bytes per entry): twice the 99th
+    // percentile slice (>= 2048, <= 49152 entries); only the longer tail goes to
+    // the grid path, so a few Zipf-heavy slices do not shrink every CTA's occupancy.
+    uint64_t cap = std::min<uint64_t>(mx, 49152);
     if (lens.size() > 100) {
       const size_t q = lens.size() - 1 - lens.size() / 100;
       std::nth_element(lens.begin(), lens.begin() + q, lens.end());

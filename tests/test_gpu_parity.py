@@ -413,7 +413,8 @@ def test_cpp_host_api(ntc, tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("lens", [(37, 1000, 9000, 23000), (40000, 12000, 3), (90000, 70000, 5, 14000)])
+@pytest.mark.parametrize("lens", [(37, 1000, 9000, 23000), (40000, 12000, 3), (90000, 70000, 5, 14000),
+                                  (1024, 1025, 1, 2, 1023) + tuple(range(700, 3700, 20))])
 def test_production_mask_equals_pick_sets(ntc, orc, lens):
     """The update kernel's sampled set (k_sample_set / heavy-slice path) is
     exactly the set of the reference's partial Fisher-Yates picks."""
