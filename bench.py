@@ -291,7 +291,7 @@ def run_ours(args, cfgd, cid):
     if not distributed:
         Fh = [np.ascontiguousarray(ctx.get_factor(m)[0]) for m in range(order)]
         outs = [(np.zeros_like(f), np.zeros_like(f)) for f in Fh]
-        ld = (R + 3) // 4 * 4
+        ld = ctx.factor_device_ptr(0, 0)[1]
         h2d = sum(d * ld * 4 for d in dims)
         d2h = 2 * h2d
         t0 = time.perf_counter()

@@ -49,6 +49,8 @@ struct HostState {
   uint64_t pending_accessed = 0;
   bool verified[NTCB_MAX_ORDER] = {};  // factor rows known nonnegative
   std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, uint64_t> bs_cache;
+  float* stage = nullptr;  // pinned fp32 staging for host-buffer factor transfers
+  uint64_t stage_n = 0;    // floats
 };
 std::map<const ntcb_context*, HostState> g_host;
 
@@ -121,8 +123,34 @@ void prof_end(ntcb_context* ctx, cudaStream_t st) {
 // Queue one s_nmc on rows [r0, r1) of `mode` with a_init == factors[mode].
 // Sampling runs on the side stream (it never reads factors), so the sample of
 // the next mode overlaps this mode's update; events order mask reuse.
+// Sampled set of inner iteration `l` into the next mask of `mode` (side
+// stream); returns the parity used.  The main stream waits on it later.
+int enqueue_sample(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, const ntcb_nmc_config& cfg,
+                   uint64_t rng_state, int l) {
+  const int par = ctx->mask_parity[mode];
+  ctx->mask_parity[mode] ^= 1;
+  const DeviceView& v = ctx->views[mode];
+  const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
+  if (cfg.c < 1.0 && e1 > e0) {
+    uint32_t* mask = ctx->mask[mode][par];
+    const uint64_t root = fork64(rng_state, static_cast<uint64_t>(l));
+    if (ctx->consumed_valid[mode][par])
+      NTCB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_consumed[mode][par], 0));
+    const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
+    NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->side));
+    prof_mark(ctx, 1, ctx->side);
+    uint64_t cap = 0;
+    ctx->prof.launches += launch_sample_set(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, &cap);
+    ctx->prof.launches += launch_sample_heavy(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, cap);
+    prof_end(ctx, ctx->side);
+    NTCB_CUDA(cudaEventRecord(ctx->ev_sampled[mode][par], ctx->side));
+  }
+  return par;
+}
+
+// presampled >= 0: the parity enqueue_sample already filled for l = 0.
 void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
-                  const ntcb_nmc_config& cfg, uint64_t rng_state) {
+                  const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
   const uint64_t ld = ctx->ld;
   cudaStream_t st = ctx->stream;
   if (r1 <= r0) return;
@@ -132,23 +160,10 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   const DeviceView& v = ctx->views[mode];
   const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
   for (int l = 0; l < cfg.max_inner; ++l) {
-    const uint64_t root = fork64(rng_state, static_cast<uint64_t>(l));
-    const int par = ctx->mask_parity[mode];
-    ctx->mask_parity[mode] ^= 1;
+    const int par = (l == 0 && presampled >= 0) ? presampled
+                                                : enqueue_sample(ctx, mode, r0, r1, cfg, rng_state, l);
     uint32_t* mask = ctx->mask[mode][par];
-    if (cfg.c < 1.0 && e1 > e0) {
-      if (ctx->consumed_valid[mode][par])
-        NTCB_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_consumed[mode][par], 0));
-      const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
-      NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->side));
-      prof_mark(ctx, 1, ctx->side);
-      uint64_t cap = 0;
-      ctx->prof.launches += launch_sample_set(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, &cap);
-      ctx->prof.launches += launch_sample_heavy(ctx, ctx->side, mask, mode, r0, r1, cfg.c, root, 0, cap);
-      prof_end(ctx, ctx->side);
-      NTCB_CUDA(cudaEventRecord(ctx->ev_sampled[mode][par], ctx->side));
-      NTCB_CUDA(cudaStreamWaitEvent(st, ctx->ev_sampled[mode][par], 0));
-    }
+    if (cfg.c < 1.0 && e1 > e0) NTCB_CUDA(cudaStreamWaitEvent(st, ctx->ev_sampled[mode][par], 0));
     prof_mark(ctx, 0, st);
     const int n = launch_update(ctx, mode, r0, r1, cfg, mask);
     ctx->prof.launches += n;
@@ -185,6 +200,54 @@ void collect(ntcb_context* ctx, uint64_t* accessed) {
     fail(NTCB_ERUNTIME, "row_step: step constant below lambda");
   }
   if (accessed) *accessed += pend;
+}
+
+float* host_stage(ntcb_context* ctx, uint64_t n) {
+  auto& hs = g_host[ctx];
+  if (hs.stage_n < n) {
+    if (hs.stage) cudaFreeHost(hs.stage);
+    hs.stage = nullptr;
+    hs.stage_n = 0;
+    NTCB_CUDA(cudaMallocHost(&hs.stage, sizeof(float) * n));
+    hs.stage_n = n;
+  }
+  return hs.stage;
+}
+
+// host doubles -> pinned fp32 rows (ld stride, zero padding) -> async H2D on
+// the main stream; false (nothing enqueued) when a value is negative or NaN
+bool upload_factor_async(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
+  const uint64_t R = ctx->rank, ld = ctx->ld;
+  float* tmp = host_stage(ctx, rows * ld);
+  bool ok = true;
+  for (uint64_t i = 0; i < rows; ++i) {
+    const double* s = src + i * R;
+    float* d = tmp + i * ld;
+    for (uint64_t r = 0; r < R; ++r) {
+      ok &= s[r] >= 0.0;
+      d[r] = static_cast<float>(s[r]);
+    }
+    for (uint64_t r = R; r < ld; ++r) d[r] = 0.f;
+  }
+  if (!ok) return false;
+  NTCB_CUDA(cudaMemcpyAsync(dst, tmp, sizeof(float) * rows * ld, cudaMemcpyHostToDevice, ctx->stream));
+  return true;
+}
+
+// A and/or Y of `mode` -> pinned staging (one sync) -> host doubles
+void download_factors(ntcb_context* ctx, int mode, double* a, double* y) {
+  const uint64_t R = ctx->rank, ld = ctx->ld, rows = ctx->dims[mode], n = rows * ld;
+  float* tmp = host_stage(ctx, 2 * n);
+  if (a) NTCB_CUDA(cudaMemcpyAsync(tmp, ctx->A[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (y) NTCB_CUDA(cudaMemcpyAsync(tmp + n, ctx->Y[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int w = 0; w < 2; ++w) {
+    double* dst = w ? y : a;
+    if (!dst) continue;
+    const float* src = tmp + w * n;
+    for (uint64_t i = 0; i < rows; ++i)
+      for (uint64_t r = 0; r < R; ++r) dst[i * R + r] = static_cast<double>(src[i * ld + r]);
+  }
 }
 
 void upload_factor(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
@@ -228,9 +291,12 @@ void alloc_factors(ntcb_context* ctx, uint64_t rank) {
   need_tensor(ctx);
   free_factors(ctx);
   ctx->rank = rank;
-  ctx->ld = (rank + 3) / 4 * 4;
+  // row stride: whole 32-byte sectors up to rank 31 (the tensor-core update
+  // gathers feature blocks of 8), 16-byte multiples above
+  ctx->ld = rank <= 31 ? (rank + 7) / 8 * 8 : (rank + 3) / 4 * 4;
   for (int m = 0; m < ctx->order; ++m) {
-    const size_t bytes = sizeof(float) * ctx->dims[m] * ctx->ld;
+    // + 32 floats: the tensor-core gather of the last row may read past it
+    const size_t bytes = sizeof(float) * (ctx->dims[m] * ctx->ld + 32);
     NTCB_CUDA(cudaMalloc(&ctx->A[m], bytes));
     NTCB_CUDA(cudaMalloc(&ctx->Y[m], bytes));
     NTCB_CUDA(cudaMemsetAsync(ctx->A[m], 0, bytes, ctx->stream));
@@ -309,6 +375,7 @@ int ntcb_destroy(ntcb_context* ctx) {
     for (auto& e : mm) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
+  if (g_host[ctx].stage) cudaFreeHost(g_host[ctx].stage);
   g_host.erase(ctx);
   delete ctx;
   API_CATCH
@@ -534,8 +601,7 @@ int ntcb_factor_get(ntcb_context* ctx, int mode, double* a, double* y) {
   need_ctx(ctx);
   need_factors(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_get: mode out of range");
-  if (a) download_factor(ctx, ctx->A[mode], a, ctx->dims[mode]);
-  if (y) download_factor(ctx, ctx->Y[mode], y, ctx->dims[mode]);
+  download_factors(ctx, mode, a, y);
   API_CATCH
 }
 
@@ -557,16 +623,21 @@ int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc
   need_factors(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
   auto& hs = g_host[ctx];
-  if (a_init) {
-    if (!all_nonneg(a_init, ctx->dims[mode] * ctx->rank))
-      fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
-    upload_factor(ctx, ctx->A[mode], a_init, ctx->dims[mode]);
-    hs.verified[mode] = true;
-  } else if (!hs.verified[mode]) {
-    fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
-  }
+  if (!a_init && !hs.verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   collect(ctx, nullptr);  // drain anything queued before
-  enqueue_snmc(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state);
+  int pre = -1;
+  if (a_init) {
+    // the first sample does not read factors: it runs on the side stream
+    // while a_init is converted and copied in
+    if (cfg->max_inner > 0) pre = enqueue_sample(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, 0);
+    if (!upload_factor_async(ctx, ctx->A[mode], a_init, ctx->dims[mode])) {
+      hs.verified[mode] = false;
+      collect(ctx, nullptr);
+      fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+    }
+    hs.verified[mode] = true;
+  }
+  enqueue_snmc(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, pre);
   collect(ctx, entries_accessed);
   API_CATCH
 }

@@ -381,6 +381,17 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
 // (longest first) through a device cursor, so CTAs stay busy to the end.
 // ---------------------------------------------------------------------------
 constexpr int kCtaThreads = 256;
+
+// 32-bit shared-window accesses: keeps the table base in one register
+// instead of re-deriving the window from the CTA id at every access
+__device__ __forceinline__ uint32_t ld_s(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_s(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 constexpr uint32_t kWarpCap = 1024;  // slices up to this length: warp per slice
 
 struct CtaArgs {
@@ -420,19 +431,29 @@ __global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
     for (uint32_t w = tid; w < pw; w += kCtaThreads) t4[w] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     // ---- phase 1: T[r_j] = max(j + 1) over draws j with r_j != j ------------
+    // (r_j == j stores max(T, 0): a no-op, so the atomic is unconditional).
+    // A draw can need Lemire's rejection loop only if lo64(x * bound) < bound,
+    // which requires the low word of u to be 0: track the minimum of those
+    // words and replay the slice exactly if it ever hits 0 (p ~ b / 2^32).
     {
-      bool rej = false;
+      uint32_t minu = 0xffffffffu;
       uint64_t s = state0 + static_cast<uint64_t>(tid + 1) * kGolden;
-      for (uint32_t j = tid; j < b; j += kCtaThreads, s += kCtaThreads * kGolden) {
+      auto draw = [&](uint32_t j, uint64_t st) {
         const uint32_t bound = n - j;
-        const uint64_t x = mix64(s);
+        const uint64_t x = mix64(st);
         const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
         const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
-        rej |= static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound;
+        minu = min(minu, static_cast<uint32_t>(u));
         const uint32_t r = j + static_cast<uint32_t>(u >> 32);
-        if (r != j) atomicMax(&T[r], j + 1);
+        atomicMax(&T[r], r != j ? j + 1 : 0u);
+      };
+      uint32_t j = tid;
+      for (; j + kCtaThreads < b; j += 2 * kCtaThreads, s += 2 * kCtaThreads * kGolden) {
+        draw(j, s);
+        draw(j + kCtaThreads, s + kCtaThreads * kGolden);
       }
-      if (rej) s_rej = 1;
+      if (j < b) draw(j, s);
+      if (minu == 0u) s_rej = 1;
     }
     __syncthreads();
     if (s_rej) {  // rare: a draw may need Lemire's rejection loop -- exact serial replay
@@ -460,42 +481,63 @@ __global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
       }
       __syncthreads();
     }
-    // ---- phase 2a: positions [b, n): picked iff targeted; flag unpicked roots
+    // ---- phase 2a: positions [b, n): picked iff targeted; flag unpicked roots.
+    // Warp w takes words kb0 + w + NW*i; lane i keeps the ballot of its i-th
+    // word, so each word costs one LDS + one VOTE and the stores go out once
+    // per 32 words.
     uint32_t* gm = a.mask + (beg >> 5);
     const int off0 = static_cast<int>(beg & 31u);
-    const int kb0 = (static_cast<int>(b) + off0) >> 5;
-    const int kend = (static_cast<int>(n) + off0 - 1) >> 5;
-    for (int k = kb0 + wid; k <= kend; k += NW) {
-      const int t = 32 * k - off0 + lane;
-      const bool valid = t >= static_cast<int>(b) && t < static_cast<int>(n);
-      const uint32_t tv = valid ? (T[t] & VAL) : 0u;
-      if (tv) {
-        uint32_t v = tv - 1, nx;
-        while ((nx = T[v] & VAL) != 0u) v = nx - 1;
-        T[v] = FLAG;  // roots hold 0: the flag alone (concurrent walkers mask it off)
-      }
-      const uint32_t bits = __ballot_sync(kFull, tv != 0u);
-      if (lane == 0) {
-        const bool whole = 32 * k - off0 >= static_cast<int>(b) && 32 * k - off0 + 32 <= static_cast<int>(n);
-        if (whole)
-          gm[k] = bits;
-        else if (bits)
-          atomicOr(&gm[k], bits);
+    uint32_t tb;  // opaque copy: ptxas would otherwise re-derive it per access
+    asm volatile("mov.u32 %0, %1;" : "=r"(tb) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(T))));
+    {
+      const int kb0 = (static_cast<int>(b) + off0) >> 5;
+      const int kend = (static_cast<int>(n) + off0 - 1) >> 5;
+      const uint32_t span = n - b;
+      for (int base = kb0 + wid; base <= kend; base += 32 * NW) {
+        uint32_t mine = 0;
+        const int cnt = min(32, (kend - base) / NW + 1);
+        int t = 32 * base - off0 + lane;
+        for (int i = 0; i < cnt; ++i, t += 32 * NW) {
+          const uint32_t tv = static_cast<uint32_t>(t - static_cast<int>(b)) < span ? (ld_s(tb + 4u * t) & VAL) : 0u;
+          if (tv) {
+            uint32_t a4 = tb + 4u * (tv - 1), nx;
+            while ((nx = ld_s(a4) & VAL) != 0u) a4 = tb + 4u * (nx - 1);
+            st_s(a4, FLAG);  // roots hold 0: the flag alone (concurrent walkers mask it off)
+          }
+          const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+          if (lane == i) mine = bits;
+        }
+        if (lane < cnt) {
+          const int k = base + NW * lane;
+          const int p0 = 32 * k - off0;
+          if (p0 >= static_cast<int>(b) && p0 + 32 <= static_cast<int>(n))
+            gm[k] = mine;
+          else if (mine)
+            atomicOr(&gm[k], mine);
+        }
       }
     }
     __syncthreads();
     // ---- phase 2b: values [0, b): picked unless flagged -----------------------
-    const int kbend = (static_cast<int>(b) + off0 - 1) >> 5;
-    for (int k = wid; k <= kbend; k += NW) {
-      const int t = 32 * k - off0 + lane;
-      const bool pick = t >= 0 && t < static_cast<int>(b) && !(T[t] & FLAG);
-      const uint32_t bits = __ballot_sync(kFull, pick);
-      if (lane == 0) {
-        const bool whole = 32 * k - off0 >= 0 && 32 * k - off0 + 32 <= static_cast<int>(b);
-        if (whole)
-          gm[k] = bits;
-        else if (bits)
-          atomicOr(&gm[k], bits);
+    {
+      const int kbend = (static_cast<int>(b) + off0 - 1) >> 5;
+      for (int base = wid; base <= kbend; base += 32 * NW) {
+        uint32_t mine = 0;
+        const int cnt = min(32, (kbend - base) / NW + 1);
+        int t = 32 * base - off0 + lane;
+        for (int i = 0; i < cnt; ++i, t += 32 * NW) {
+          const bool pick = static_cast<uint32_t>(t) < b && !(ld_s(tb + 4u * t) & FLAG);
+          const uint32_t bits = __ballot_sync(kFull, pick);
+          if (lane == i) mine = bits;
+        }
+        if (lane < cnt) {
+          const int k = base + NW * lane;
+          const int p0 = 32 * k - off0;
+          if (p0 >= 0 && p0 + 32 <= static_cast<int>(b))
+            gm[k] = mine;
+          else if (mine)
+            atomicOr(&gm[k], mine);
+        }
       }
     }
     __syncthreads();

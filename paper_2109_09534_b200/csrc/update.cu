@@ -28,6 +28,7 @@
 // (nmc.cpp:174-197).  fp32 accumulation; sums are taken in slice order over
 // the (bit-exact) sampled set.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -61,6 +62,7 @@ struct UpdateArgs {
   int no;                              // order - 1
   int mode;
   int rank;
+  int ld;                              // factor row stride (floats)
   float* A;
   float* Y;
   const WorkItem* items;
@@ -126,12 +128,11 @@ __device__ __forceinline__ void block_of(int blk, int nb4, int& bi, int& bj) {
 
 // Warp-level finalisation of one row from Hf (R x HS, fp32 sums of k k^T,
 // full symmetric) and g (fp64 sums of s k, in gd).  Writes A[p], Y[p].
-template <int LD4>
 __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv,
                              int lane) {
   const int R = a.rank;
   const int HS = R | 1;
-  const int ld = LD4 * 4;
+  const int ld = a.ld;
   const double lam = a.lambda;
   // On entry gd holds w = sum_e x_e k_e.  grad = sum_e (y.k_e - x_e) k_e + lambda y
   // = H y - w + lambda y with H = sum k k^T (nmc.cpp:84-105).  Forming it here
@@ -515,7 +516,336 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
     }
     __syncwarp();
     if (w.slot < 0) {
-      finalize_row<LD4>(a, p, Hf, gd, vv, lane);
+      finalize_row(a, p, Hf, gd, vv, lane);
+    } else {
+      float* dst = a.partial + static_cast<uint64_t>(w.slot) * (R * R + R);
+      for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
+      for (int r = lane; r < R; r += 32) dst[R * R + r] = static_cast<float>(gd[r]);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core Gram (ranks with R + 1 <= 8P, P <= 4).
+//
+// The Gram sum_e k_e k_e^T and w = sum_e x_e k_e are one matrix product:
+// with k'_e = (k_e, x_e, 0...) (8P features) and K the picks x 8P matrix,
+// K^T K holds H in its leading R x R block and w in column R.  A warp
+// multiplies 8 picks at a time with mma.sync (m16n8), upper block tiles
+// only (n-tile j >= 2 m-tile i).  fp32 accuracy from two products per tile:
+//   k = hi + lo, hi = k with the low 13 mantissa bits cleared (exact tf32),
+//   tf32  mma:  hi hi^T                        (exact products)
+//   bf16  mma:  hi lo^T + lo hi^T               (k16 = 8 picks x {hi, lo})
+// The dropped lo lo^T and the bf16 rounding of the cross terms are
+// <= 2^-18 of |k_a k_b| per pick -- the size of fp32 accumulation error.
+//
+// Fragment ownership: lane (g = lane/4, t = lane%4) holds picks 2t, 2t+1 of
+// the group and features rho = g + 8f (f < P) of both.  For the tf32
+// product k-index t <-> pick 2t and t+4 <-> pick 2t+1; for the bf16 product
+// k-index 2t/2t+1 <-> hi of picks 2t/2t+1 and 2t+8/2t+9 <-> their lo.
+// ---------------------------------------------------------------------------
+template <int P>
+struct TcGeo {
+  static constexpr int MT = (P + 1) / 2;  // m-tiles (16 features)
+  static constexpr int NT = P == 1 ? 1 : P == 2 ? 2 : P == 3 ? 4 : 6;  // sum_i (P - 2i)
+  static constexpr int mi(int tile) {  // m-tile of a tile index
+    return P <= 2 ? 0 : (P == 3 ? (tile < 3 ? 0 : 1) : (tile < 4 ? 0 : 1));
+  }
+  static constexpr int nj(int tile) {  // n-tile of a tile index
+    return P <= 2 ? tile : (P == 3 ? (tile < 3 ? tile : 2) : (tile < 4 ? tile : tile - 2));
+  }
+};
+
+__device__ __forceinline__ void mma_tf32(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two floats -> bf16x2, `lo_k` in the low half (the smaller k index)
+__device__ __forceinline__ uint32_t pack_bf16(float lo_k, float hi_k) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;\n" : "=r"(d) : "f"(hi_k), "f"(lo_k));
+  return d;
+}
+
+template <int P, int NO>
+__global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
+  using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
+  using G = TcGeo<P>;
+  constexpr int GP = 8;  // picks per group
+  extern __shared__ __align__(16) float smem_f[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int no = NO < NTCB_MAX_ORDER - 1 ? NO : a.no;
+  const int R = a.rank;
+  const int HS = R | 1;
+  const int ld = a.ld;
+  float* wbase = smem_f + static_cast<size_t>(wid) * W::words(no, R);
+  uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
+  float* st_x = wbase + no * W::kStage;                 // [kStage]
+  float* Hf = wbase + W::stage_words(no);               // [R][HS]
+  double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));  // [64]
+  double* vv = gd + 64;                                             // [64]
+  uint32_t* rbat = reinterpret_cast<uint32_t*>(vv + 64);            // raw batches
+  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                       // [2][32]
+  const bool full = a.c >= 1.0;
+  const int g = lane >> 2;
+  const int q0 = 2 * (lane & 3);  // this lane's picks: q0, q0 + 1
+  constexpr int NP = P / 2;       // feature-block pairs
+  // feature of (lane group gg, block f) -- the rho -> feature map of K'
+  auto feat = [&](int gg, int f) { return f < 2 * NP ? 16 * (f / 2) + 2 * gg + (f & 1) : 16 * NP + gg; };
+  int xf = -1;  // block in which this lane holds the x column (feature R)
+#pragma unroll
+  for (int f = 0; f < P; ++f)
+    if (feat(g, f) == R) xf = f;
+  const uint32_t ld4 = static_cast<uint32_t>(ld) * 4u;
+  const float* ub2[NO];
+  const float* ub1[NO];
+#pragma unroll
+  for (int m = 0; m < NO; ++m) {
+    ub2[m] = a.U[m < no ? m : 0] + 2 * g;
+    ub1[m] = a.U[m < no ? m : 0] + 16 * NP + g;
+  }
+
+  while (true) {
+    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(&a.counters[2], 1ull);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const WorkItem w = a.items[it];
+    const uint64_t p = w.row;
+
+    float acc[G::NT][4];
+#pragma unroll
+    for (int i = 0; i < G::NT; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+
+    int head = 0, cnt = 0;  // staging ring [head, head+cnt)
+
+    struct Raw {
+      float f[NO][2][P];  // factor values (mode, pick, feature block)
+      float x[2];
+    };
+    // gather of one group: np picks present (8 for full groups).  Block pair
+    // (2i, 2i+1) of a pick is one 8-byte load (features 16i + 2g, +1), an odd
+    // last block one 4-byte load (feature 16 NP + g); reads past R hit the
+    // row padding or the next row and land in discarded rows/cols of K'^T K'.
+    auto load = [&](int at, int np) {
+      Raw r;
+      const int s0 = (at + q0) & (W::kStage - 1), s1 = (at + q0 + 1) & (W::kStage - 1);
+      const bool on0 = q0 < np, on1 = q0 + 1 < np;
+#pragma unroll
+      for (int m = 0; m < NO; ++m)
+        if (m < no) {
+          const uint32_t rw[2] = {on0 ? st_o[m * W::kStage + s0] : 0u, on1 ? st_o[m * W::kStage + s1] : 0u};
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const char* b2 = reinterpret_cast<const char*>(ub2[m]) + static_cast<uint64_t>(rw[q]) * ld4;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+              const float2 v = __ldg(reinterpret_cast<const float2*>(b2) + 8 * i);
+              r.f[m][q][2 * i] = v.x;
+              r.f[m][q][2 * i + 1] = v.y;
+            }
+            if (P & 1) {
+              const char* b1 = reinterpret_cast<const char*>(ub1[m]) + static_cast<uint64_t>(rw[q]) * ld4;
+              r.f[m][q][P - 1] = __ldg(reinterpret_cast<const float*>(b1));
+            }
+          }
+        }
+      r.x[0] = on0 ? st_x[s0] : 0.f;
+      r.x[1] = on1 ? st_x[s1] : 0.f;
+      if (!on0)
+#pragma unroll
+        for (int f = 0; f < P; ++f) r.f[0][0][f] = 0.f;
+      if (!on1)
+#pragma unroll
+        for (int f = 0; f < P; ++f) r.f[0][1][f] = 0.f;
+      return r;
+    };
+    auto compute = [&](const Raw& r) {
+      uint32_t hb[2][P], hp[P], lp[P];
+#pragma unroll
+      for (int f = 0; f < P; ++f) {
+        float lo[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          float k = r.f[0][q][f];
+#pragma unroll
+          for (int m = 1; m < NO; ++m)
+            if (m < no) k *= r.f[m][q][f];
+          if (xf == f) k = r.x[q];  // the x column of k'
+          hb[q][f] = __float_as_uint(k) & 0xffffe000u;
+          lo[q] = k - __uint_as_float(hb[q][f]);
+        }
+        hp[f] = pack_bf16(__uint_as_float(hb[0][f]), __uint_as_float(hb[1][f]));
+        lp[f] = pack_bf16(lo[0], lo[1]);
+      }
+#pragma unroll
+      for (int tl = 0; tl < G::NT; ++tl) {
+        const int i = G::mi(tl), j = G::nj(tl);
+        const int m0 = 2 * i, m1 = 2 * i + 1;
+        const uint32_t a0 = hb[0][m0], a2 = hb[1][m0];
+        const uint32_t a1 = m1 < P ? hb[0][m1 < P ? m1 : 0] : 0u;
+        const uint32_t a3 = m1 < P ? hb[1][m1 < P ? m1 : 0] : 0u;
+        mma_tf32(acc[tl], a0, a1, a2, a3, hb[0][j], hb[1][j]);
+        const uint32_t c1 = m1 < P ? hp[m1 < P ? m1 : 0] : 0u;
+        const uint32_t c3 = m1 < P ? lp[m1 < P ? m1 : 0] : 0u;
+        mma_bf16(acc[tl], hp[m0], c1, lp[m0], c3, lp[j], hp[j]);
+      }
+    };
+    // all staged full groups, three-way rotation (two gathers in flight)
+    auto drain_full = [&]() {
+      const int ng = cnt / GP;
+      if (ng == 0) return;
+      int al = head;
+      Raw r0, r1, r2;
+      r0 = load(al, GP);
+      al = (al + GP) & (W::kStage - 1);
+      if (1 < ng) {
+        r1 = load(al, GP);
+        al = (al + GP) & (W::kStage - 1);
+      }
+      for (int gi = 0; gi < ng; gi += 3) {
+        if (gi + 2 < ng) {
+          r2 = load(al, GP);
+          al = (al + GP) & (W::kStage - 1);
+        }
+        compute(r0);
+        if (gi + 1 < ng) {
+          if (gi + 3 < ng) {
+            r0 = load(al, GP);
+            al = (al + GP) & (W::kStage - 1);
+          }
+          compute(r1);
+          if (gi + 2 < ng) {
+            if (gi + 4 < ng) {
+              r1 = load(al, GP);
+              al = (al + GP) & (W::kStage - 1);
+            }
+            compute(r2);
+          }
+        }
+      }
+      head = (head + ng * GP) & (W::kStage - 1);
+      cnt -= ng * GP;
+    };
+
+    // ---- stream the item in batches of 128 entries (as k_update) -----------
+    const uint64_t tb = w.e0 & ~uint64_t(3);
+    const int lo = static_cast<int>(w.e0 - tb);
+    const int hi = static_cast<int>(w.e1 - tb);
+    auto fetch_async = [&](int t, int buf) {
+      const int r = t + 4 * lane;
+      if (r < hi) {
+        const uint64_t e = tb + static_cast<uint64_t>(r);
+#pragma unroll
+        for (int m = 0; m < NO + 1; ++m) {
+          if (m < no || m == NO) {
+            const int row = (m == NO) ? no : m;
+            const void* src = (m == NO) ? static_cast<const void*>(a.val + e) : static_cast<const void*>(a.oth[m] + e);
+            const unsigned dst = static_cast<unsigned>(
+                __cvta_generic_to_shared(rbat + (buf * (no + 1) + row) * 128 + 4 * lane));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+          }
+        }
+        if (!full) {
+          const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + lane));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dm), "l"(a.mask + (e >> 5)));
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    const uint32_t sh0 = static_cast<uint32_t>(tb & 31u);
+    fetch_async(0, 0);
+    int buf = 0;
+    for (int t0 = 0; t0 < hi; t0 += 128, buf ^= 1) {
+      if (t0 + 128 < hi) {
+        fetch_async(t0 + 128, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::);
+      }
+      uint4 co[NO];
+#pragma unroll
+      for (int m = 0; m < NO; ++m)
+        if (m < no) co[m] = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + m) * 128)[lane];
+      const uint4 cv = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + no) * 128)[lane];
+      const int r = t0 + 4 * lane;
+      uint32_t bits = full ? 0xfu : (rmsk[buf * 32 + lane] >> ((sh0 + static_cast<uint32_t>(r)) & 31u)) & 0xfu;
+      if (r < lo) bits &= 0xfu << (lo - r);
+      if (r + 4 > hi) bits &= hi - r > 0 ? (0xfu >> (4 - (hi - r))) : 0u;
+      const int c4 = __popc(bits);
+      int incl = c4;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int slot = head + cnt + incl - c4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if ((bits >> q) & 1u) {
+          const int sl = slot & (W::kStage - 1);
+#pragma unroll
+          for (int m = 0; m < NO; ++m)
+            if (m < no) st_o[m * W::kStage + sl] = q == 0 ? co[m].x : q == 1 ? co[m].y : q == 2 ? co[m].z : co[m].w;
+          st_x[sl] = __uint_as_float(q == 0 ? cv.x : q == 1 ? cv.y : q == 2 ? cv.z : cv.w);
+          ++slot;
+        }
+      }
+      cnt += total;
+      __syncwarp();
+      drain_full();
+    }
+    if (cnt > 0) {  // the item's last, partial group
+      const Raw rp = load(head, cnt);
+      compute(rp);
+      head = (head + cnt) & (W::kStage - 1);
+      cnt = 0;
+    }
+
+    // ---- accumulators -> Hf (mirrored upper triangle) and w ----------------
+    __syncwarp();
+#pragma unroll
+    for (int tl = 0; tl < G::NT; ++tl) {
+      const int i = G::mi(tl), j = G::nj(tl);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int fb = 2 * i + ((e & 2) ? 1 : 0);  // row block
+        const int gc = 2 * (lane & 3) + (e & 1);   // col lane group
+        const int rho_r = 8 * fb + g, rho_c = 8 * j + gc;
+        if (fb >= P || rho_r > rho_c) continue;  // each unordered pair once
+        const int fr = feat(g, fb), fc = feat(gc, j);
+        const float v = acc[tl][e];
+        if (fr < R && fc < R) {
+          Hf[fr * HS + fc] = v;
+          Hf[fc * HS + fr] = v;
+        } else if (fr < R && fc == R) {
+          gd[fr] = static_cast<double>(v);
+        } else if (fc < R && fr == R) {
+          gd[fc] = static_cast<double>(v);
+        }
+      }
+    }
+    __syncwarp();
+    if (w.slot < 0) {
+      finalize_row(a, p, Hf, gd, vv, lane);
     } else {
       float* dst = a.partial + static_cast<uint64_t>(w.slot) * (R * R + R);
       for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
@@ -554,7 +884,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
       gd[r] = s;
     }
     __syncwarp();
-    finalize_row<LD4>(a, fi.row, Hf, gd, vv, lane);
+    finalize_row(a, fi.row, Hf, gd, vv, lane);
     __syncwarp();
   }
 }
@@ -640,12 +970,42 @@ static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, si
   return 1;
 }
 
+template <int P, int NO>
+static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  int per_sm = 0;
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO>, kWarps * 32, smem));
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (pl.n_items + kWarps - 1) / kWarps;
+  grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+  grid = std::max<uint64_t>(grid, 1);
+  k_update_tc<P, NO><<<static_cast<unsigned>(grid), kWarps * 32, smem, ctx->stream>>>(a);
+  NTCB_CUDA(cudaGetLastError());
+  return 1;
+}
+
+template <int P>
+static int launch_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
+  if (a.no == 1) return launch_items_tc<P, 1>(ctx, a, pl, smem);
+  if (a.no == 2) return launch_items_tc<P, 2>(ctx, a, pl, smem);
+  return launch_items_tc<P, 3>(ctx, a, pl, smem);
+}
+
+static bool g_tc_off = std::getenv("NTCB_NO_TC") != nullptr;  // A/B switch: CUDA-core Gram
+
 template <int LD4>
 static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   using W = WarpSmem<LD4>;
   const size_t smem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 * kWarps;
   int launches = 0;
-  if (pl.n_items) {
+  const int P = (a.rank + 1 + 7) / 8;  // feature blocks of k' = (k, x)
+  if (pl.n_items && P <= 4 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
+    launches += P == 1 ? launch_tc<1>(ctx, a, pl, smem)
+              : P == 2 ? launch_tc<2>(ctx, a, pl, smem)
+              : P == 3 ? launch_tc<3>(ctx, a, pl, smem)
+                       : launch_tc<4>(ctx, a, pl, smem);
+  } else if (pl.n_items) {
     if (a.no == 2)
       launches += launch_items<LD4, 2>(ctx, a, pl, smem);
     else if (a.no == 3)
@@ -694,6 +1054,7 @@ int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_
   a.mask = mask;
   a.mode = mode;
   a.rank = static_cast<int>(R);
+  a.ld = static_cast<int>(ctx->ld);
   a.A = ctx->A[mode];
   a.Y = ctx->Y[mode];
   a.items = pl.d_items;
