@@ -580,6 +580,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_k, float hi_k) {
   return d;
 }
 
+// base + row * ld4 bytes as one wide multiply-add
+__device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row, uint32_t ld4) {
+  uint64_t p;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(row), "r"(ld4), "l"(reinterpret_cast<uint64_t>(base)));
+  return reinterpret_cast<const float*>(p);
+}
+
 template <int P, int NO>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
@@ -604,8 +611,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
   const int g = lane >> 2;
   const int q0 = 2 * (lane & 3);  // this lane's picks: q0, q0 + 1
   constexpr int NP = P / 2;       // feature-block pairs
+  constexpr bool QUAD = P == 4;   // ld == 32: one 128-byte row per pick and mode
   // feature of (lane group gg, block f) -- the rho -> feature map of K'
-  auto feat = [&](int gg, int f) { return f < 2 * NP ? 16 * (f / 2) + 2 * gg + (f & 1) : 16 * NP + gg; };
+  auto feat = [&](int gg, int f) {
+    return QUAD ? 4 * gg + f : (f < 2 * NP ? 16 * (f / 2) + 2 * gg + (f & 1) : 16 * NP + gg);
+  };
   int xf = -1;  // block in which this lane holds the x column (feature R)
 #pragma unroll
   for (int f = 0; f < P; ++f)
@@ -615,7 +625,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
   const float* ub1[NO];
 #pragma unroll
   for (int m = 0; m < NO; ++m) {
-    ub2[m] = a.U[m < no ? m : 0] + 2 * g;
+    ub2[m] = a.U[m < no ? m : 0] + (QUAD ? 4 * g : 2 * g);
     ub1[m] = a.U[m < no ? m : 0] + 16 * NP + g;
   }
 
@@ -640,35 +650,46 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
       float f[NO][2][P];  // factor values (mode, pick, feature block)
       float x[2];
     };
-    // gather of one group: np picks present (8 for full groups).  Block pair
-    // (2i, 2i+1) of a pick is one 8-byte load (features 16i + 2g, +1), an odd
-    // last block one 4-byte load (feature 16 NP + g); reads past R hit the
-    // row padding or the next row and land in discarded rows/cols of K'^T K'.
+    // gather of one group: np picks present (8 for full groups).  Quad layout
+    // (P = 4, ld = 32): one 16-byte load per pick and mode, features 4g..4g+3
+    // (a row is one 128-byte line).  Pair layout (P <= 3): block pair
+    // (2i, 2i+1) is one 8-byte load (features 16i + 2g, +1), an odd last
+    // block one 4-byte load (feature 16 NP + g).  Reads past R hit the row
+    // padding or the next row and land in discarded rows/cols of K'^T K'.
+    // Group starts are multiples of 8 (head only advances by whole groups
+    // inside an item), so the ring pair (q0, q0 + 1) is one 8-byte load.
     auto load = [&](int at, int np) {
       Raw r;
-      const int s0 = (at + q0) & (W::kStage - 1), s1 = (at + q0 + 1) & (W::kStage - 1);
+      const int s0 = (at + q0) & (W::kStage - 1);
       const bool on0 = q0 < np, on1 = q0 + 1 < np;
 #pragma unroll
       for (int m = 0; m < NO; ++m)
         if (m < no) {
-          const uint32_t rw[2] = {on0 ? st_o[m * W::kStage + s0] : 0u, on1 ? st_o[m * W::kStage + s1] : 0u};
+          const uint2 rr = *reinterpret_cast<const uint2*>(st_o + m * W::kStage + s0);
+          const uint32_t rw[2] = {on0 ? rr.x : 0u, on1 ? rr.y : 0u};
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const char* b2 = reinterpret_cast<const char*>(ub2[m]) + static_cast<uint64_t>(rw[q]) * ld4;
+            const float* b2 = row_ptr(ub2[m], rw[q], ld4);
+            if (QUAD) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(b2));
+              r.f[m][q][0] = v.x;
+              r.f[m][q][1 % P] = v.y;
+              r.f[m][q][2 % P] = v.z;
+              r.f[m][q][3 % P] = v.w;
+            } else {
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
-              const float2 v = __ldg(reinterpret_cast<const float2*>(b2) + 8 * i);
-              r.f[m][q][2 * i] = v.x;
-              r.f[m][q][2 * i + 1] = v.y;
-            }
-            if (P & 1) {
-              const char* b1 = reinterpret_cast<const char*>(ub1[m]) + static_cast<uint64_t>(rw[q]) * ld4;
-              r.f[m][q][P - 1] = __ldg(reinterpret_cast<const float*>(b1));
+              for (int i = 0; i < NP; ++i) {
+                const float2 v = __ldg(reinterpret_cast<const float2*>(b2) + 8 * i);
+                r.f[m][q][2 * i] = v.x;
+                r.f[m][q][2 * i + 1] = v.y;
+              }
+              if (P & 1) r.f[m][q][P - 1] = __ldg(row_ptr(ub1[m], rw[q], ld4));
             }
           }
         }
-      r.x[0] = on0 ? st_x[s0] : 0.f;
-      r.x[1] = on1 ? st_x[s1] : 0.f;
+      const float2 xx = *reinterpret_cast<const float2*>(st_x + s0);
+      r.x[0] = on0 ? xx.x : 0.f;
+      r.x[1] = on1 ? xx.y : 0.f;
       if (!on0)
 #pragma unroll
         for (int f = 0; f < P; ++f) r.f[0][0][f] = 0.f;
@@ -746,7 +767,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
     };
 
     // ---- stream the item in batches of 128 entries (as k_update) -----------
-    const uint64_t tb = w.e0 & ~uint64_t(3);
+    const uint64_t tb = w.e0 & ~uint64_t(31);  // 128-byte aligned: one line per quarter-warp cp.async
     const int lo = static_cast<int>(w.e0 - tb);
     const int hi = static_cast<int>(w.e1 - tb);
     auto fetch_async = [&](int t, int buf) {
@@ -999,8 +1020,10 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   using W = WarpSmem<LD4>;
   const size_t smem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 * kWarps;
   int launches = 0;
-  const int P = (a.rank + 1 + 7) / 8;  // feature blocks of k' = (k, x)
-  if (pl.n_items && P <= 4 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
+  // feature blocks of k' = (k, x), pair layout (the 16-byte quad layout reads
+  // whole 128-byte rows and measured 40% slower at rank 20)
+  const int P = (a.rank + 1 + 7) / 8;
+  if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
     launches += P == 1 ? launch_tc<1>(ctx, a, pl, smem)
               : P == 2 ? launch_tc<2>(ctx, a, pl, smem)
               : P == 3 ? launch_tc<3>(ctx, a, pl, smem)
