@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -214,21 +215,38 @@ float* host_stage(ntcb_context* ctx, uint64_t n) {
   return hs.stage;
 }
 
+// f(row_begin, row_end) over [0, rows) on up to 16 host threads (large factors only)
+template <class F>
+bool parallel_rows(uint64_t rows, uint64_t per_row, F f) {
+  const uint64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const uint64_t nt = std::min<uint64_t>({hw, 16, std::max<uint64_t>(1, rows * per_row / (1 << 19))});
+  if (nt <= 1) return f(0, rows);
+  std::vector<std::thread> th;
+  std::vector<char> ok(nt, 1);
+  for (uint64_t t = 0; t < nt; ++t)
+    th.emplace_back([&, t] { ok[t] = f(rows * t / nt, rows * (t + 1) / nt); });
+  for (auto& x : th) x.join();
+  return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+}
+
 // host doubles -> pinned fp32 rows (ld stride, zero padding) -> async H2D on
 // the main stream; false (nothing enqueued) when a value is negative or NaN
 bool upload_factor_async(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
   const uint64_t R = ctx->rank, ld = ctx->ld;
   float* tmp = host_stage(ctx, rows * ld);
-  bool ok = true;
-  for (uint64_t i = 0; i < rows; ++i) {
-    const double* s = src + i * R;
-    float* d = tmp + i * ld;
-    for (uint64_t r = 0; r < R; ++r) {
-      ok &= s[r] >= 0.0;
-      d[r] = static_cast<float>(s[r]);
+  const bool ok = parallel_rows(rows, R, [&](uint64_t i0, uint64_t i1) {
+    bool good = true;
+    for (uint64_t i = i0; i < i1; ++i) {
+      const double* s = src + i * R;
+      float* d = tmp + i * ld;
+      for (uint64_t r = 0; r < R; ++r) {
+        good &= s[r] >= 0.0;
+        d[r] = static_cast<float>(s[r]);
+      }
+      for (uint64_t r = R; r < ld; ++r) d[r] = 0.f;
     }
-    for (uint64_t r = R; r < ld; ++r) d[r] = 0.f;
-  }
+    return good;
+  });
   if (!ok) return false;
   NTCB_CUDA(cudaMemcpyAsync(dst, tmp, sizeof(float) * rows * ld, cudaMemcpyHostToDevice, ctx->stream));
   return true;
@@ -241,13 +259,16 @@ void download_factors(ntcb_context* ctx, int mode, double* a, double* y) {
   if (a) NTCB_CUDA(cudaMemcpyAsync(tmp, ctx->A[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
   if (y) NTCB_CUDA(cudaMemcpyAsync(tmp + n, ctx->Y[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int w = 0; w < 2; ++w) {
-    double* dst = w ? y : a;
-    if (!dst) continue;
-    const float* src = tmp + w * n;
-    for (uint64_t i = 0; i < rows; ++i)
-      for (uint64_t r = 0; r < R; ++r) dst[i * R + r] = static_cast<double>(src[i * ld + r]);
-  }
+  parallel_rows(rows, 2 * R, [&](uint64_t i0, uint64_t i1) {
+    for (int w = 0; w < 2; ++w) {
+      double* dst = w ? y : a;
+      if (!dst) continue;
+      const float* src = tmp + w * n;
+      for (uint64_t i = i0; i < i1; ++i)
+        for (uint64_t r = 0; r < R; ++r) dst[i * R + r] = static_cast<double>(src[i * ld + r]);
+    }
+    return true;
+  });
 }
 
 void upload_factor(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
