@@ -580,6 +580,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_k, float hi_k) {
   return d;
 }
 
+// per-warp shared words of k_update_tc: staging ring + batch landing zone,
+// the latter reused for (Hf, gd, vv) at the row end
+__host__ __device__ constexpr int tc_words(int no, int R) {
+  return WarpSmem<1>::stage_words(no) + (WarpSmem<1>::batch_words(no) > WarpSmem<1>::ktile_words(R) + 256
+                                             ? WarpSmem<1>::batch_words(no)
+                                             : WarpSmem<1>::ktile_words(R) + 256);
+}
+
 // base + row * ld4 bytes as one wide multiply-add
 __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row, uint32_t ld4) {
   uint64_t p;
@@ -599,14 +607,15 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
   const int R = a.rank;
   const int HS = R | 1;
   const int ld = a.ld;
-  float* wbase = smem_f + static_cast<size_t>(wid) * W::words(no, R);
+  float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R);
   uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
   float* st_x = wbase + no * W::kStage;                 // [kStage]
-  float* Hf = wbase + W::stage_words(no);               // [R][HS]
+  uint32_t* rbat = reinterpret_cast<uint32_t*>(wbase + W::stage_words(no));  // raw batches
+  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                                // [2][32]
+  // the row-end buffers alias the batch landing zone (idle once an item is streamed)
+  float* Hf = wbase + W::stage_words(no);                           // [R][HS]
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));  // [64]
   double* vv = gd + 64;                                             // [64]
-  uint32_t* rbat = reinterpret_cast<uint32_t*>(vv + 64);            // raw batches
-  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                       // [2][32]
   const bool full = a.c >= 1.0;
   const int g = lane >> 2;
   const int q0 = 2 * (lane & 3);  // this lane's picks: q0, q0 + 1
@@ -1024,10 +1033,11 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // whole 128-byte rows and measured 40% slower at rank 20)
   const int P = (a.rank + 1 + 7) / 8;
   if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
-    launches += P == 1 ? launch_tc<1>(ctx, a, pl, smem)
-              : P == 2 ? launch_tc<2>(ctx, a, pl, smem)
-              : P == 3 ? launch_tc<3>(ctx, a, pl, smem)
-                       : launch_tc<4>(ctx, a, pl, smem);
+    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank)) * 4 * kWarps;
+    launches += P == 1 ? launch_tc<1>(ctx, a, pl, ts)
+              : P == 2 ? launch_tc<2>(ctx, a, pl, ts)
+              : P == 3 ? launch_tc<3>(ctx, a, pl, ts)
+                       : launch_tc<4>(ctx, a, pl, ts);
   } else if (pl.n_items) {
     if (a.no == 2)
       launches += launch_items<LD4, 2>(ctx, a, pl, smem);
