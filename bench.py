@@ -280,6 +280,19 @@ def run_ours(args, cfgd, cid):
     per_launch_bytes = alg_bytes / order
     avg_upd_s = (upd_ms / max(upd_launches, 1)) / 1000.0
     achieved = per_launch_bytes / avg_upd_s / 1e9
+    # compute side: reference-formulation FLOPs per sampled nnz
+    # 2[(N-2)R + 3R + R(R+1)/2] plus ~8R per processed row (power iterations not
+    # counted), against the CUDA-core FP32 peak measured on this pool
+    # (tools/microbench/hmma.cu: 70.8 TFLOP/s FFMA)
+    alg_flops = 2 * ((N - 2) * R + 3 * R + R * (R + 1) // 2) * full + 8 * R * rows_processed
+    flops_launch = alg_flops / order
+    fp32_peak = 70.8
+    compute = {"alg_flops_per_launch": flops_launch,
+               "achieved_tflops": flops_launch / avg_upd_s / 1e12,
+               "fp32_peak_tflops": fp32_peak, "fp32_peak_source": "measured FFMA, tools/microbench/hmma.cu",
+               "frac_fp32": flops_launch / avg_upd_s / 1e12 / fp32_peak}
+    limiter = ("L1/LSU data pipe: two factor-row gathers from L2 per sampled nnz (ncu: LSU wavefronts "
+               "80% of peak, DRAM 11%; profiles/r01_v9_k_update_tc.txt); Gram on tensor cores")
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json")
     if os.path.exists(tp):
@@ -372,7 +385,8 @@ def run_ours(args, cfgd, cid):
                          "alg_bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": avg_upd_s * 1000.0,
                          "sampler_ms_per_step": smp_ms / args.steps,
-                         "update_ms_per_step": upd_ms / args.steps},
+                         "update_ms_per_step": upd_ms / args.steps,
+                         "compute": compute, "limiter": limiter},
             "clocks": clocks, "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu,
         }
