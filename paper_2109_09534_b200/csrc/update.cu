@@ -548,12 +548,21 @@ __global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(Upda
 template <int P>
 struct TcGeo {
   static constexpr int MT = (P + 1) / 2;  // m-tiles (16 features)
-  static constexpr int NT = P == 1 ? 1 : P == 2 ? 2 : P == 3 ? 4 : 6;  // sum_i (P - 2i)
-  static constexpr int mi(int tile) {  // m-tile of a tile index
-    return P <= 2 ? 0 : (P == 3 ? (tile < 3 ? 0 : 1) : (tile < 4 ? 0 : 1));
+  static constexpr int count() {           // upper block tiles: sum_i (P - 2i)
+    int n = 0;
+    for (int i = 0; i < MT; ++i) n += P - 2 * i;
+    return n;
   }
-  static constexpr int nj(int tile) {  // n-tile of a tile index
-    return P <= 2 ? tile : (P == 3 ? (tile < 3 ? tile : 2) : (tile < 4 ? tile : tile - 2));
+  static constexpr int NT = count();
+  static constexpr int mi(int tl) {  // m-tile of a tile index
+    int i = 0;
+    while (tl >= P - 2 * i) tl -= P - 2 * i++;
+    return i;
+  }
+  static constexpr int nj(int tl) {  // n-tile of a tile index
+    int i = 0;
+    while (tl >= P - 2 * i) tl -= P - 2 * i++;
+    return 2 * i + tl;
   }
 };
 
@@ -596,7 +605,7 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
 }
 
 template <int P, int NO>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
   constexpr int GP = 8;  // picks per group
@@ -630,6 +639,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_update_tc(UpdateArgs a) {
   for (int f = 0; f < P; ++f)
     if (feat(g, f) == R) xf = f;
   const uint32_t ld4 = static_cast<uint32_t>(ld) * 4u;
+
   const float* ub2[NO];
   const float* ub1[NO];
 #pragma unroll
@@ -1032,6 +1042,9 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // feature blocks of k' = (k, x), pair layout (the 16-byte quad layout reads
   // whole 128-byte rows and measured 40% slower at rank 20)
   const int P = (a.rank + 1 + 7) / 8;
+  // ranks 32-39 (P = 5) compile but stay on the CUDA-core kernel: at one CTA
+  // per SM the pair-layout gathers of three factors measured 21 ms vs 17.6 ms
+  // per mode on config 4
   if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
     const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank)) * 4 * kWarps;
     launches += P == 1 ? launch_tc<1>(ctx, a, pl, ts)

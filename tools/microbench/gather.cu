@@ -37,6 +37,28 @@ __global__ void __launch_bounds__(256, 2) k(const float* __restrict__ U, const u
         const float* b = U + (size_t)r[2 * t + q] * LD;
         acc += __ldg(b + g) + __ldg(b + g + 8) * __ldg(b + g + 16);
       }
+    } else if (V == 5) {  // natural float4 (8 lanes per 128-byte row) + SHFL into the fragment layout
+      float4 v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float* b = U + (size_t)r[4 * h + (lane >> 3)] * LD;
+        v[h] = __ldg(reinterpret_cast<const float4*>(b) + (lane & 7));
+      }
+      // lane (g,t) wants picks t and t+4, features 4g + f (f = 0..3): register f of lane 8t + g
+      const int src = 8 * t + g;
+      float f0 = __shfl_sync(0xffffffffu, v[0].x, src), f1 = __shfl_sync(0xffffffffu, v[0].y, src);
+      float f2 = __shfl_sync(0xffffffffu, v[0].z, src), f3 = __shfl_sync(0xffffffffu, v[0].w, src);
+      float e0 = __shfl_sync(0xffffffffu, v[1].x, src), e1 = __shfl_sync(0xffffffffu, v[1].y, src);
+      float e2 = __shfl_sync(0xffffffffu, v[1].z, src), e3 = __shfl_sync(0xffffffffu, v[1].w, src);
+      acc += f0 * f1 + f2 * f3 + e0 * e1 + e2 * e3;
+    } else if (V == 6) {  // natural float4, no transposition (reference for V5)
+      float4 v[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float* b = U + (size_t)r[4 * h + (lane >> 3)] * LD;
+        v[h] = __ldg(reinterpret_cast<const float4*>(b) + (lane & 7));
+      }
+      acc += v[0].x * v[0].y + v[0].z * v[0].w + v[1].x * v[1].y + v[1].z * v[1].w;
     } else if (V == 4) {  // natural float2: 12 lanes per row (2.67 rows per instr) -> 16 lanes per row, 2 rows per instr
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
@@ -85,6 +107,8 @@ int main() {
   run(k<4, 24>, "natural ld24 float2");
   run(k<1, 32>, "pair ld32");
   run(k<2, 32>, "natural ld32 float4");
+  run(k<5, 32>, "natural ld32 float4 + 8 SHFL");
+  run(k<6, 32>, "natural ld32 float4 (V5 w/o SHFL)");
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
