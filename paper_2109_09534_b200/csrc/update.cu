@@ -949,16 +949,21 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   std::vector<WorkItem> items;
   std::vector<FinItem> fins;
   int64_t slot = 0;
+  // Segment length: at most kSeg, and short enough that the range yields ~4
+  // items per resident warp (a row shard of a multi-GPU run has few rows).
+  const uint64_t target = 4ull * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps;
+  const uint64_t total = off[r1] - off[r0];
+  const uint64_t seg = std::min<uint64_t>(kSeg, std::max<uint64_t>(2048, (total / target + 127) / 128 * 128));
   for (uint64_t p = r0; p < r1; ++p) {
     const uint64_t n = off[p + 1] - off[p];
     if (blocksize_for(c, n) == 0) continue;  // skipped row (nmc.cpp:237)
-    if (n <= kSeg) {
+    if (n <= seg) {
       items.push_back({p, off[p], off[p + 1], -1});
     } else {
-      const uint64_t ns = (n + kSeg - 1) / kSeg;
+      const uint64_t ns = (n + seg - 1) / seg;
       fins.push_back({p, slot, static_cast<int32_t>(ns)});
       for (uint64_t s = 0; s < ns; ++s)
-        items.push_back({p, off[p] + s * kSeg, std::min(off[p + 1], off[p] + (s + 1) * kSeg), slot++});
+        items.push_back({p, off[p] + s * seg, std::min(off[p + 1], off[p] + (s + 1) * seg), slot++});
     }
   }
   // longest items first: better tail balance for the dynamic scheduler
