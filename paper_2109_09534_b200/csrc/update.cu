@@ -953,7 +953,9 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   // items per resident warp (a row shard of a multi-GPU run has few rows).
   const uint64_t target = 4ull * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps;
   const uint64_t total = off[r1] - off[r0];
-  const uint64_t seg = std::min<uint64_t>(kSeg, std::max<uint64_t>(2048, (total / target + 127) / 128 * 128));
+  // (small ranges keep whole rows: an extra k_finalize launch costs more there)
+  const uint64_t seg = total < (4ull << 20) ? kSeg
+                     : std::min<uint64_t>(kSeg, std::max<uint64_t>(2048, (total / target + 127) / 128 * 128));
   for (uint64_t p = r0; p < r1; ++p) {
     const uint64_t n = off[p + 1] - off[p];
     if (blocksize_for(c, n) == 0) continue;  // skipped row (nmc.cpp:237)
