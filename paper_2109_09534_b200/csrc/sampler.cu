@@ -380,7 +380,6 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
 // are separated by __syncthreads.  Slices are taken from a host-built list
 // (longest first) through a device cursor, so CTAs stay busy to the end.
 // ---------------------------------------------------------------------------
-constexpr int kCtaThreads = 256;
 
 // 32-bit shared-window accesses: keeps the table base in one register
 // instead of re-deriving the window from the CTA id at every access
@@ -405,6 +404,7 @@ struct CtaArgs {
   unsigned long long* cursor;    // zeroed before the launch
 };
 
+template <int kCtaThreads>
 __global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
   constexpr uint32_t FLAG = 0x80000000u, VAL = 0x7fffffffu;
   constexpr int NW = kCtaThreads / 32;
@@ -544,12 +544,18 @@ __global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
   }
 }
 
-// Per (view, row range, cap): how many short slices, and the mid-slice list.
+// Per (view, row range, cap): how many short slices, and the mid-slice lists
+// in two size buckets (small tables -> many CTAs per SM; large tables -> 1024
+// threads per slice), longest first.
+constexpr uint32_t kMidSplit = 16384;
+struct SampleBucket {
+  uint32_t* rows = nullptr;
+  uint32_t n = 0;
+  uint32_t max_len = 0;
+};
 struct SamplePlan {
   uint64_t n_short = 0;
-  uint32_t* mid = nullptr;
-  uint32_t n_mid = 0;
-  uint32_t max_mid = 0;
+  SampleBucket mid[2];
 };
 static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, SamplePlan> g_splans;
 
@@ -558,25 +564,43 @@ static const SamplePlan& sample_plan(const DeviceView& v, uint64_t r0, uint64_t 
   auto it = g_splans.find(key);
   if (it != g_splans.end()) return it->second;
   SamplePlan pl;
-  std::vector<std::pair<uint64_t, uint32_t>> mid;
+  std::vector<std::pair<uint64_t, uint32_t>> mid[2];
   for (uint64_t p = r0; p < r1; ++p) {
     const uint64_t n = v.h_off[p + 1] - v.h_off[p];
     if (n < 2) continue;  // b = floor(c n) = 0 for c < 1
     if (n <= kWarpCap)
       ++pl.n_short;
     else if (n <= cap)
-      mid.emplace_back(n, static_cast<uint32_t>(p));
+      mid[n > kMidSplit].emplace_back(n, static_cast<uint32_t>(p));
   }
-  std::stable_sort(mid.begin(), mid.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-  if (!mid.empty()) {
-    std::vector<uint32_t> rows(mid.size());
-    for (size_t i = 0; i < mid.size(); ++i) rows[i] = mid[i].second;
-    NTCB_CUDA(cudaMalloc(&pl.mid, sizeof(uint32_t) * rows.size()));
-    NTCB_CUDA(cudaMemcpy(pl.mid, rows.data(), sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice));
-    pl.n_mid = static_cast<uint32_t>(rows.size());
-    pl.max_mid = static_cast<uint32_t>(mid.front().first);
+  for (int k = 0; k < 2; ++k) {
+    auto& m = mid[k];
+    std::stable_sort(m.begin(), m.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    if (m.empty()) continue;
+    std::vector<uint32_t> rows(m.size());
+    for (size_t i = 0; i < m.size(); ++i) rows[i] = m[i].second;
+    NTCB_CUDA(cudaMalloc(&pl.mid[k].rows, sizeof(uint32_t) * rows.size()));
+    NTCB_CUDA(cudaMemcpy(pl.mid[k].rows, rows.data(), sizeof(uint32_t) * rows.size(), cudaMemcpyHostToDevice));
+    pl.mid[k].n = static_cast<uint32_t>(rows.size());
+    pl.mid[k].max_len = static_cast<uint32_t>(m.front().first);
   }
   return g_splans.emplace(key, pl).first->second;
+}
+
+template <int T>
+static void launch_cta_bucket(ntcb_context* ctx, cudaStream_t stream, const SampleBucket& bk, CtaArgs a) {
+  a.rows = bk.rows;
+  a.n_rows = bk.n;
+  const size_t smem = (static_cast<size_t>(bk.max_len) * 4 + 15) / 16 * 16;
+  NTCB_CUDA(cudaFuncSetAttribute(k_sample_cta<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  int per_sm = 0;
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_cta<T>, T, smem));
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t grid = std::min<uint64_t>(bk.n, static_cast<uint64_t>(per_sm) * ctx->sm_count);
+  NTCB_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), stream));
+  k_sample_cta<T><<<static_cast<unsigned>(grid), T, smem, stream>>>(a);
+  NTCB_CUDA(cudaGetLastError());
 }
 
 // Short slices on the warp kernel, mid slices on the CTA kernel; returns the
@@ -590,7 +614,7 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
   if (v.max_slice >= (1ull << 31))
     fail(NTCB_EINVAL, "sampler: slices of 2^31 or more entries are not supported");
   // shared-memory cap of the CTA kernel: u32 per entry, <= 48K entries
-  uint64_t cap = std::min<uint64_t>(v.max_slice, v.light_cap ? v.light_cap : 49152);
+  uint64_t cap = std::min<uint64_t>(v.max_slice, 49152);
   if (cap < kWarpCap) cap = kWarpCap;
   if (heavy_cap) *heavy_cap = cap;
   const SamplePlan& pl = sample_plan(v, row_begin, row_end, cap);
@@ -618,27 +642,21 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
     NTCB_CUDA(cudaGetLastError());
     ++launches;
   }
-  if (pl.n_mid) {
+  for (int k = 0; k < 2; ++k) {
+    if (!pl.mid[k].n) continue;
     if (direct) fail(NTCB_EINVAL, "sampler: direct streams are single-slice (warp kernel)");
     CtaArgs a{};
     a.off = v.off;
-    a.rows = pl.mid;
-    a.n_rows = pl.n_mid;
     a.c = c;
     a.root = root;
     a.mask = mask;
     a.counters = ctx->counters;
-    a.cursor = ctx->counters + (stream == ctx->side ? 4 : 5);
-    const size_t smem = (static_cast<size_t>(pl.max_mid) * 4 + 15) / 16 * 16;
-    NTCB_CUDA(cudaFuncSetAttribute(k_sample_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    int per_sm = 0;
-    NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_cta, kCtaThreads, smem));
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t grid = std::min<uint64_t>(pl.n_mid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
-    NTCB_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), stream));
-    k_sample_cta<<<static_cast<unsigned>(grid), kCtaThreads, smem, stream>>>(a);
-    NTCB_CUDA(cudaGetLastError());
+    // one cursor per (stream, bucket): the buckets run back to back on one stream
+    a.cursor = ctx->counters + (stream == ctx->side ? 4 : 6) + k;
+    if (k == 0)
+      launch_cta_bucket<256>(ctx, stream, pl.mid[k], a);
+    else
+      launch_cta_bucket<1024>(ctx, stream, pl.mid[k], a);
     ++launches;
   }
   return launches;
@@ -650,7 +668,8 @@ void drop_sample_plans(ntcb_context* ctx) {
     for (int m = 0; m < NTCB_MAX_ORDER; ++m)
       if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
     if (mine) {
-      if (it->second.mid) cudaFree(it->second.mid);
+      for (auto& b : it->second.mid)
+        if (b.rows) cudaFree(b.rows);
       it = g_splans.erase(it);
     } else {
       ++it;
