@@ -481,64 +481,51 @@ __global__ void __launch_bounds__(kCtaThreads) k_sample_cta(CtaArgs a) {
       }
       __syncthreads();
     }
-    // ---- phase 2a: positions [b, n): picked iff targeted; flag unpicked roots.
-    // Warp w takes words kb0 + w + NW*i; lane i keeps the ballot of its i-th
-    // word, so each word costs one LDS + one VOTE and the stores go out once
-    // per 32 words.
-    uint32_t* gm = a.mask + (beg >> 5);
+    // ---- phase 2: a shared bitmap of the slice (word k covers relative
+    // positions [32k - off0, 32k - off0 + 32)), pre-set to the values [0, b).
+    // Positions t in [b, n) set their bit iff targeted (T[t] != 0) and clear
+    // the bit of the unpicked root of their chain (a value < b); the two
+    // kinds of bit never share a position, so OR and AND commute.  Then one
+    // coalesced flush; only the slice's first and last words are shared with
+    // neighbouring slices (atomicOr).
     const int off0 = static_cast<int>(beg & 31u);
-    uint32_t tb;  // opaque copy: ptxas would otherwise re-derive it per access
-    asm volatile("mov.u32 %0, %1;" : "=r"(tb) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(T))));
+    const int nw = (off0 + static_cast<int>(n) + 31) >> 5;
+    uint32_t* SB = T + ((n + 3) & ~3u);  // after the table
+    for (int k = tid; k < nw; k += kCtaThreads) {
+      const int p0 = 32 * k - off0;  // relative position of bit 0
+      const int lo_ = p0 < 0 ? -p0 : 0;                                   // first bit inside the slice
+      const int hiv = static_cast<int>(b) - p0;                           // bits below b
+      const uint32_t below = hiv <= 0 ? 0u : hiv >= 32 ? 0xffffffffu : ((1u << hiv) - 1u);
+      SB[k] = below & (0xffffffffu << lo_);
+    }
+    __syncthreads();
     {
+      uint32_t tb;  // opaque copy: ptxas would otherwise re-derive it per access
+      asm volatile("mov.u32 %0, %1;" : "=r"(tb) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(T))));
       const int kb0 = (static_cast<int>(b) + off0) >> 5;
-      const int kend = (static_cast<int>(n) + off0 - 1) >> 5;
+      const int kend = nw - 1;
       const uint32_t span = n - b;
-      for (int base = kb0 + wid; base <= kend; base += 32 * NW) {
-        uint32_t mine = 0;
-        const int cnt = min(32, (kend - base) / NW + 1);
-        int t = 32 * base - off0 + lane;
-        for (int i = 0; i < cnt; ++i, t += 32 * NW) {
-          const uint32_t tv = static_cast<uint32_t>(t - static_cast<int>(b)) < span ? (ld_s(tb + 4u * t) & VAL) : 0u;
-          if (tv) {
-            uint32_t a4 = tb + 4u * (tv - 1), nx;
-            while ((nx = ld_s(a4) & VAL) != 0u) a4 = tb + 4u * (nx - 1);
-            st_s(a4, FLAG);  // roots hold 0: the flag alone (concurrent walkers mask it off)
-          }
-          const uint32_t bits = __ballot_sync(kFull, tv != 0u);
-          if (lane == i) mine = bits;
+      for (int k = kb0 + wid; k <= kend; k += NW) {
+        const int t = 32 * k - off0 + lane;
+        const uint32_t tv = static_cast<uint32_t>(t - static_cast<int>(b)) < span ? (ld_s(tb + 4u * t) & VAL) : 0u;
+        if (tv) {
+          uint32_t a4 = tb + 4u * (tv - 1), nx;
+          while ((nx = ld_s(a4) & VAL) != 0u) a4 = tb + 4u * (nx - 1);
+          const uint32_t v = (a4 - tb) >> 2;  // the unpicked root (< b)
+          atomicAnd(&SB[(static_cast<uint32_t>(off0) + v) >> 5], ~(1u << ((static_cast<uint32_t>(off0) + v) & 31u)));
         }
-        if (lane < cnt) {
-          const int k = base + NW * lane;
-          const int p0 = 32 * k - off0;
-          if (p0 >= static_cast<int>(b) && p0 + 32 <= static_cast<int>(n))
-            gm[k] = mine;
-          else if (mine)
-            atomicOr(&gm[k], mine);
-        }
+        const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+        if (lane == 0 && bits) atomicOr(&SB[k], bits);
       }
     }
     __syncthreads();
-    // ---- phase 2b: values [0, b): picked unless flagged -----------------------
-    {
-      const int kbend = (static_cast<int>(b) + off0 - 1) >> 5;
-      for (int base = wid; base <= kbend; base += 32 * NW) {
-        uint32_t mine = 0;
-        const int cnt = min(32, (kbend - base) / NW + 1);
-        int t = 32 * base - off0 + lane;
-        for (int i = 0; i < cnt; ++i, t += 32 * NW) {
-          const bool pick = static_cast<uint32_t>(t) < b && !(ld_s(tb + 4u * t) & FLAG);
-          const uint32_t bits = __ballot_sync(kFull, pick);
-          if (lane == i) mine = bits;
-        }
-        if (lane < cnt) {
-          const int k = base + NW * lane;
-          const int p0 = 32 * k - off0;
-          if (p0 >= 0 && p0 + 32 <= static_cast<int>(b))
-            gm[k] = mine;
-          else if (mine)
-            atomicOr(&gm[k], mine);
-        }
-      }
+    uint32_t* gm = a.mask + (beg >> 5);
+    for (int k = tid; k < nw; k += kCtaThreads) {
+      const uint32_t v = SB[k];
+      if (k != 0 && k != nw - 1)
+        gm[k] = v;
+      else if (v)
+        atomicOr(&gm[k], v);
     }
     __syncthreads();
   }
@@ -591,7 +578,8 @@ template <int T>
 static void launch_cta_bucket(ntcb_context* ctx, cudaStream_t stream, const SampleBucket& bk, CtaArgs a) {
   a.rows = bk.rows;
   a.n_rows = bk.n;
-  const size_t smem = (static_cast<size_t>(bk.max_len) * 4 + 15) / 16 * 16;
+  // u32 table (padded to 16 bytes) + the slice bitmap (off0 + n bits)
+  const size_t smem = (static_cast<size_t>(bk.max_len) + 3) / 4 * 16 + ((bk.max_len + 31) / 32 + 2) * 4;
   NTCB_CUDA(cudaFuncSetAttribute(k_sample_cta<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
