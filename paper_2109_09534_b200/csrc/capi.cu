@@ -5,8 +5,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -215,17 +219,81 @@ float* host_stage(ntcb_context* ctx, uint64_t n) {
   return hs.stage;
 }
 
-// f(row_begin, row_end) over [0, rows) on up to 16 host threads (large factors only)
+// A persistent host worker pool for the fp64 <-> fp32 factor conversions of
+// the host-buffer entry points (spawning threads per call costs more than the
+// conversion of a 10^4 x 20 factor).  Leaked on purpose: it must outlive any
+// static destructor that could still run a conversion.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // run f(t) for t in [0, n) (n <= size()); the caller runs t = 0
+  void run(int n, const std::function<void(int)>& f) {
+    if (n <= 1) {
+      f(0);
+      return;
+    }
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      job_ = &f;
+      jobs_ = n;
+      next_ = 1;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    unsigned n = std::min(hw, 16u) - 1;
+    if (const char* e = std::getenv("NTCB_HOST_THREADS")) n = std::max(1, std::atoi(e)) - 1;  // A/B knob
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto& w : workers_) w.detach();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    while (true) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      while (job_ && next_ < jobs_) {
+        const int t = next_++;
+        const std::function<void(int)>* f = job_;
+        lk.unlock();
+        (*f)(t);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int jobs_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// f(row_begin, row_end) over [0, rows), split over the pool for large factors
 template <class F>
 bool parallel_rows(uint64_t rows, uint64_t per_row, F f) {
-  const uint64_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const uint64_t nt = std::min<uint64_t>({hw, 16, std::max<uint64_t>(1, rows * per_row / (1 << 19))});
+  HostPool& pool = HostPool::get();
+  const uint64_t nt = std::min<uint64_t>(pool.size(), std::max<uint64_t>(1, rows * per_row / (1 << 15)));
   if (nt <= 1) return f(0, rows);
-  std::vector<std::thread> th;
   std::vector<char> ok(nt, 1);
-  for (uint64_t t = 0; t < nt; ++t)
-    th.emplace_back([&, t] { ok[t] = f(rows * t / nt, rows * (t + 1) / nt); });
-  for (auto& x : th) x.join();
+  const std::function<void(int)> job = [&](int t) {
+    ok[t] = f(rows * t / nt, rows * (t + 1) / nt);
+  };
+  pool.run(static_cast<int>(nt), job);
   return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
 }
 
