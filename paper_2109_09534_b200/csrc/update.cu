@@ -589,12 +589,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo_k, float hi_k) {
   return d;
 }
 
-// per-warp shared words of k_update_tc: staging ring + batch landing zone,
-// the latter reused for (Hf, gd, vv) at the row end
+// per-warp shared words of k_update_tc: the staging ring (reused for Hf, gd,
+// vv at the row end, when the ring is drained) + the batch landing zone (free
+// at the row end, so the next item's first batch lands there meanwhile)
+__host__ __device__ constexpr int tc_ring_words(int no, int R) {
+  return WarpSmem<1>::stage_words(no) > WarpSmem<1>::ktile_words(R) + 256 ? WarpSmem<1>::stage_words(no)
+                                                                          : WarpSmem<1>::ktile_words(R) + 256;
+}
 __host__ __device__ constexpr int tc_words(int no, int R) {
-  return WarpSmem<1>::stage_words(no) + (WarpSmem<1>::batch_words(no) > WarpSmem<1>::ktile_words(R) + 256
-                                             ? WarpSmem<1>::batch_words(no)
-                                             : WarpSmem<1>::ktile_words(R) + 256);
+  return tc_ring_words(no, R) + WarpSmem<1>::batch_words(no);
 }
 
 // base + row * ld4 bytes as one wide multiply-add
@@ -619,10 +622,10 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
   float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R);
   uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
   float* st_x = wbase + no * W::kStage;                 // [kStage]
-  uint32_t* rbat = reinterpret_cast<uint32_t*>(wbase + W::stage_words(no));  // raw batches
-  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                                // [2][32]
-  // the row-end buffers alias the batch landing zone (idle once an item is streamed)
-  float* Hf = wbase + W::stage_words(no);                           // [R][HS]
+  uint32_t* rbat = reinterpret_cast<uint32_t*>(wbase + tc_ring_words(no, R));  // raw batches
+  uint32_t* rmsk = rbat + 2 * (no + 1) * 128;                                  // [2][32]
+  // the row-end buffers alias the staging ring (drained once an item is streamed)
+  float* Hf = wbase;                                                // [R][HS]
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));  // [64]
   double* vv = gd + 64;                                             // [64]
   const bool full = a.c >= 1.0;
@@ -648,13 +651,52 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     ub1[m] = a.U[m < no ? m : 0] + 16 * NP + g;
   }
 
-  while (true) {
-    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+  // Record batches of an item: 128 entries from tb + t into buffer buf
+  // (cp.async 16-byte copies of oth[.] and val, the mask word; one group).
+  auto fetch_async = [&](uint64_t tb, int hi, int t, int buf) {
+    const int r = t + 4 * lane;
+    if (r < hi) {
+      const uint64_t e = tb + static_cast<uint64_t>(r);
+#pragma unroll
+      for (int m = 0; m < NO + 1; ++m) {
+        if (m < no || m == NO) {
+          const int row = (m == NO) ? no : m;
+          const void* src = (m == NO) ? static_cast<const void*>(a.val + e) : static_cast<const void*>(a.oth[m] + e);
+          const unsigned dst = static_cast<unsigned>(
+              __cvta_generic_to_shared(rbat + (buf * (no + 1) + row) * 128 + 4 * lane));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+        }
+      }
+      if (!full) {
+        const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + lane));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dm), "l"(a.mask + (e >> 5)));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  // Items are prefetched one ahead: the next item's index is claimed while the
+  // current one streams, and its first batch is copied in while the current
+  // row is finalised (short rows are otherwise a chain of exposed latencies).
+  auto claim = [&]() {
     unsigned long long it = 0;
     if (lane == 0) it = atomicAdd(&a.counters[2], 1ull);
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= a.n_items) break;
-    const WorkItem w = a.items[it];
+    return it;  // lane 0 only; broadcast when needed
+  };
+  auto begin_item = [&](unsigned long long it, WorkItem& w) {
+    if (it >= a.n_items) return false;
+    w = a.items[it];
+    const uint64_t tb = w.e0 & ~uint64_t(31);  // 128-byte aligned: one line per quarter-warp cp.async
+    fetch_async(tb, static_cast<int>(w.e1 - tb), 0, 0);
+    return true;
+  };
+  WorkItem w;
+  bool have = begin_item(__shfl_sync(0xffffffffu, claim(), 0), w);
+  while (have) {
+    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      return;
+    }
+    const unsigned long long next_it = claim();
     const uint64_t p = w.row;
 
     float acc[G::NT][4];
@@ -785,37 +827,16 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       cnt -= ng * GP;
     };
 
-    // ---- stream the item in batches of 128 entries (as k_update) -----------
-    const uint64_t tb = w.e0 & ~uint64_t(31);  // 128-byte aligned: one line per quarter-warp cp.async
+    // ---- stream the item in batches of 128 entries (as k_update); batch 0
+    // is already in flight (begin_item) ----------------------------------------
+    const uint64_t tb = w.e0 & ~uint64_t(31);
     const int lo = static_cast<int>(w.e0 - tb);
     const int hi = static_cast<int>(w.e1 - tb);
-    auto fetch_async = [&](int t, int buf) {
-      const int r = t + 4 * lane;
-      if (r < hi) {
-        const uint64_t e = tb + static_cast<uint64_t>(r);
-#pragma unroll
-        for (int m = 0; m < NO + 1; ++m) {
-          if (m < no || m == NO) {
-            const int row = (m == NO) ? no : m;
-            const void* src = (m == NO) ? static_cast<const void*>(a.val + e) : static_cast<const void*>(a.oth[m] + e);
-            const unsigned dst = static_cast<unsigned>(
-                __cvta_generic_to_shared(rbat + (buf * (no + 1) + row) * 128 + 4 * lane));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
-          }
-        }
-        if (!full) {
-          const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + lane));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dm), "l"(a.mask + (e >> 5)));
-        }
-      }
-      asm volatile("cp.async.commit_group;\n" ::);
-    };
     const uint32_t sh0 = static_cast<uint32_t>(tb & 31u);
-    fetch_async(0, 0);
     int buf = 0;
     for (int t0 = 0; t0 < hi; t0 += 128, buf ^= 1) {
       if (t0 + 128 < hi) {
-        fetch_async(t0 + 128, buf ^ 1);
+        fetch_async(tb, hi, t0 + 128, buf ^ 1);
         asm volatile("cp.async.wait_group 1;\n" ::);
       } else {
         asm volatile("cp.async.wait_group 0;\n" ::);
@@ -859,9 +880,12 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       head = (head + cnt) & (W::kStage - 1);
       cnt = 0;
     }
+    // next item: its first batch lands while this row is finalised
+    const WorkItem cur = w;
+    __syncwarp();
+    have = begin_item(__shfl_sync(0xffffffffu, next_it, 0), w);
 
     // ---- accumulators -> Hf (mirrored upper triangle) and w ----------------
-    __syncwarp();
 #pragma unroll
     for (int tl = 0; tl < G::NT; ++tl) {
       const int i = G::mi(tl), j = G::nj(tl);
@@ -884,10 +908,10 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       }
     }
     __syncwarp();
-    if (w.slot < 0) {
+    if (cur.slot < 0) {
       finalize_row(a, p, Hf, gd, vv, lane);
     } else {
-      float* dst = a.partial + static_cast<uint64_t>(w.slot) * (R * R + R);
+      float* dst = a.partial + static_cast<uint64_t>(cur.slot) * (R * R + R);
       for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
       for (int r = lane; r < R; r += 32) dst[R * R + r] = static_cast<float>(gd[r]);
     }
