@@ -1043,15 +1043,21 @@ static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, si
 
 template <int P, int NO>
 static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
+  // Few items (a small tensor or a thin row shard): fewer warps per CTA so the
+  // items spread over every SM instead of filling a few.
+  const size_t warp_bytes = smem / kWarps;
+  const uint64_t per_sm_items = (pl.n_items + 2 * ctx->sm_count - 1) / (2 * ctx->sm_count);
+  const int wpc = static_cast<int>(std::min<uint64_t>(kWarps, std::max<uint64_t>(1, per_sm_items)));
+  smem = warp_bytes * wpc;
   NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO>, kWarps * 32, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO>, wpc * 32, smem));
   if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (pl.n_items + kWarps - 1) / kWarps;
+  uint64_t grid = (pl.n_items + wpc - 1) / wpc;
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   grid = std::max<uint64_t>(grid, 1);
-  k_update_tc<P, NO><<<static_cast<unsigned>(grid), kWarps * 32, smem, ctx->stream>>>(a);
+  k_update_tc<P, NO><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
   return 1;
 }
