@@ -59,6 +59,10 @@ __host__ __device__ __forceinline__ uint64_t blocksize_for(double c, uint64_t n)
 // Entry order inside a slice is the reference's (mode_view.cpp:5-7):
 // lexicographic in the remaining coordinates.
 // ---------------------------------------------------------------------------
+// view arrays are padded so a whole 128-entry batch (512 bytes, the update's
+// bulk copy) starting at any 32-entry boundary <= nnz stays in bounds
+constexpr uint64_t kViewPad = 160;
+
 struct DeviceView {
   uint64_t rows = 0;
   uint64_t max_slice = 0;

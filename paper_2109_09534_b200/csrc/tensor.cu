@@ -281,8 +281,8 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
     DeviceView& v = ctx->views[m];
     v.rows = dims[m];
     NTCB_CUDA(cudaMalloc(&v.off, sizeof(uint64_t) * (v.rows + 1)));
-    for (int k = 0; k < order - 1; ++k) NTCB_CUDA(cudaMalloc(&v.oth[k], sizeof(uint32_t) * (nnz + 4)));
-    NTCB_CUDA(cudaMalloc(&v.val, sizeof(float) * (nnz + 4)));
+    for (int k = 0; k < order - 1; ++k) NTCB_CUDA(cudaMalloc(&v.oth[k], sizeof(uint32_t) * (nnz + kViewPad)));
+    NTCB_CUDA(cudaMalloc(&v.val, sizeof(float) * (nnz + kViewPad)));
     if (nnz) {
       NTCB_CUDA(cudaMemcpyAsync(mperm.p, perm.p, sizeof(uint32_t) * nnz, cudaMemcpyDeviceToDevice, st));
       k_mode_keys<<<grid_for(nnz, sms), 256, 0, st>>>(d_idx, mperm.p, nnz, order, m, mkey);
