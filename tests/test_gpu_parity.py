@@ -522,3 +522,53 @@ def test_ranks_and_orders_vs_oracle(ntc, orc, order, R):
             a, y = ctx.get_factor(m)
             assert rel(a, F[m]) <= TOL, (k, m, rel(a, F[m]))
             assert rel(y, M[m]) <= TOL, (k, m, rel(y, M[m]))
+
+
+def test_adaptive_segments_vs_oracle(ntc, orc):
+    """Rows of 8000 entries in a range of 8M: the work list cuts them into
+    2048-entry segments (partial slots + k_finalize) although they are below
+    the 16384-entry item cap; results against the fp64 restatement."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [1000, 2000, 2000], 8_000_000, 12
+    ctx = P.Context(0)
+    ctx.synth(dims, nnz, 6, 0.01, 4242)
+    ci, cv = ctx.canonical()
+    cv64 = cv.astype(np.float64)
+    view0 = orc.build_view(dims, ci, cv64, 0)
+    assert int(np.diff(view0[0].astype(np.int64)).max()) < 16384
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 5)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    cfg = P.NmcConfig(c=0.5)
+    st = orc.sweep_state(11, 0, 0)
+    ctx.s_nmc_rows_async(0, 0, dims[0], cfg, st)
+    acc = ctx.collect()
+    oacc = orc.s_nmc(dims, R, F, M, 0, view0, None, O.nmc_cfg(c=0.5, threads=16), st)
+    assert acc == oacc
+    a, y = ctx.get_factor(0)
+    assert rel(a, F[0]) <= TOL and rel(y, M[0]) <= TOL
+
+
+def test_host_buffers_large_factor_threads(ntc):
+    """ntcb_s_nmc_host on a 400000-row factor: the fp64<->fp32 conversions run
+    on the host worker pool; outputs equal the device state, and a negative
+    a_init entry deep in the factor (a worker's chunk) is still rejected."""
+    import paper_2109_09534_b200 as P
+    dims, R = [400_000, 30, 20], 8
+    ctx = P.Context(0)
+    ctx.synth(dims, 2_000_000, 4, 0.01, 99)
+    ctx.random_factors(R, 3)
+    a0, _ = ctx.get_factor(0)
+    a_out, y_out = np.zeros_like(a0), np.zeros_like(a0)
+    cfg = P.NmcConfig(c=0.5)
+    n = ctx.s_nmc_host(0, a0, a_out, y_out, cfg, 777)
+    assert n > 0
+    a1, y1 = ctx.get_factor(0)
+    np.testing.assert_array_equal(a_out, a1)
+    np.testing.assert_array_equal(y_out, y1)
+    bad = a1.copy()
+    bad[371_234, 5] = -1.0
+    with pytest.raises(ValueError, match="a_init must be nonnegative"):
+        ctx.s_nmc_host(0, bad, a_out, y_out, cfg, 778)
+    a2, _ = ctx.get_factor(0)
+    np.testing.assert_array_equal(a2, a1)  # rejected before anything was uploaded
