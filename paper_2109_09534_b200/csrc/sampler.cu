@@ -28,6 +28,7 @@
 // Output: one bit per view entry in `mask` (the sampled SET that the update
 // kernel streams) and optionally the picks in draw order (parity tests).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -585,6 +586,11 @@ static void launch_cta_bucket(ntcb_context* ctx, cudaStream_t stream, const Samp
   int per_sm = 0;
   NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_cta<T>, T, smem));
   if (per_sm < 1) per_sm = 1;
+  static const int side_cap = [] {
+    const char* e = std::getenv("NTCB_SIDE_SAMPLER_CTAS");  // experiment knob
+    return e ? std::atoi(e) : 0;
+  }();
+  if (stream == ctx->side && side_cap > 0) per_sm = std::min(per_sm, side_cap);
   const uint64_t grid = std::min<uint64_t>(bk.n, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   NTCB_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), stream));
   k_sample_cta<T><<<static_cast<unsigned>(grid), T, smem, stream>>>(a);
