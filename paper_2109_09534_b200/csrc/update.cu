@@ -919,10 +919,16 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
   }
 }
 
-// Rows split across several items: sum their partial slots in slot order
-// (deterministic), then the same finalisation.
+// Rows split across several items: a CTA per row sums its partial slots --
+// warp w takes the contiguous slot range w of 8, lanes the elements, every
+// load of a slot in flight at once -- then the 8 warp sums are combined in
+// warp order in shared memory (deterministic: the association depends only
+// on the slot count) and warp 0 runs the same finalisation.
+constexpr int kFinPass = 512;  // elements per pass (16 per lane)
+constexpr int kFinSmall = 16;  // rows with at most this many slots: a warp each
+
 template <int LD4>
-__global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
+__global__ void __launch_bounds__(kWarps * 32) k_finalize_small(UpdateArgs a) {
   using W = WarpSmem<LD4>;
   extern __shared__ __align__(16) float smem_f[];
   const int lane = threadIdx.x & 31;
@@ -933,23 +939,91 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
   float* Hf = wbase + W::stage_words(a.no);
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));
   double* vv = gd + 64;
+  const int NE = R * R + R;
   for (uint64_t f = blockIdx.x * kWarps + wid; f < a.n_fins; f += static_cast<uint64_t>(gridDim.x) * kWarps) {
     if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
     const FinItem fi = a.fins[f];
-    for (int i = lane; i < R * R; i += 32) {
-      float s = 0.f;
-      for (int q = 0; q < fi.nslots; ++q) s += a.partial[static_cast<uint64_t>(fi.slot0 + q) * (R * R + R) + i];
-      Hf[(i / R) * HS + (i % R)] = s;
-    }
-    for (int r = lane; r < R; r += 32) {
-      double s = 0.0;
-      for (int q = 0; q < fi.nslots; ++q)
-        s += static_cast<double>(a.partial[static_cast<uint64_t>(fi.slot0 + q) * (R * R + R) + R * R + r]);
-      gd[r] = s;
+    const float* base = a.partial + static_cast<uint64_t>(fi.slot0) * NE;
+    // slot sums in slot order; the slot loads of 4 elements per lane are in flight together
+    for (int i0 = 0; i0 < NE; i0 += 128) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < fi.nslots; q += 4) {
+        float v[4][4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u + lane;
+            v[qq][u] = (q + qq < fi.nslots && i < NE) ? base[static_cast<uint64_t>(q + qq) * NE + i] : 0.f;
+          }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(v[qq][u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        if (i < R * R)
+          Hf[(i / R) * HS + (i % R)] = static_cast<float>(acc[u]);
+        else if (i < NE)
+          gd[i - R * R] = acc[u];
+      }
     }
     __syncwarp();
     finalize_row(a, fi.row, Hf, gd, vv, lane);
     __syncwarp();
+  }
+}
+
+
+template <int LD4>
+__global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
+  using W = WarpSmem<LD4>;
+  extern __shared__ __align__(16) float smem_f[];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int R = a.rank;
+  const int HS = R | 1;
+  float* Hf = smem_f + W::stage_words(a.no);  // warp 0's row-end buffers
+  double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));
+  double* vv = gd + 64;
+  double* P = reinterpret_cast<double*>(smem_f + W::words(a.no, R));  // [kWarps][kFinPass]
+  const int NE = R * R + R;
+  for (uint64_t f = blockIdx.x; f < a.n_fins; f += gridDim.x) {
+    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+    const FinItem fi = a.fins[f];
+    const int chunk = (fi.nslots + kWarps - 1) / kWarps;
+    const int qa = wid * chunk, qb = min(fi.nslots, qa + chunk);
+    for (int e0 = 0; e0 < NE; e0 += kFinPass) {
+      double acc[kFinPass / 32];
+#pragma unroll
+      for (int u = 0; u < kFinPass / 32; ++u) acc[u] = 0.0;
+      for (int q = qa; q < qb; ++q) {
+        const float* src = a.partial + static_cast<uint64_t>(fi.slot0 + q) * NE + e0;
+        float v[kFinPass / 32];
+#pragma unroll
+        for (int u = 0; u < kFinPass / 32; ++u) v[u] = (e0 + 32 * u + lane < NE) ? src[32 * u + lane] : 0.f;
+#pragma unroll
+        for (int u = 0; u < kFinPass / 32; ++u) acc[u] += static_cast<double>(v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kFinPass / 32; ++u) P[wid * kFinPass + 32 * u + lane] = acc[u];
+      __syncthreads();
+      for (int i = threadIdx.x; i < kFinPass && e0 + i < NE; i += kWarps * 32) {
+        double t = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kWarps; ++w2) t += P[w2 * kFinPass + i];
+        const int e = e0 + i;
+        if (e < R * R)
+          Hf[(e / R) * HS + (e % R)] = static_cast<float>(t);
+        else
+          gd[e - R * R] = t;
+      }
+      __syncthreads();
+    }
+    if (wid == 0) finalize_row(a, fi.row, Hf, gd, vv, lane);
+    __syncthreads();
   }
 }
 
@@ -958,8 +1032,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
 // ---------------------------------------------------------------------------
 struct WorkPlan {
   WorkItem* d_items = nullptr;
-  FinItem* d_fins = nullptr;
-  uint64_t n_items = 0, n_fins = 0, n_slots = 0;
+  FinItem* d_fins = nullptr;  // [n_small small rows][n_fins - n_small big rows]
+  uint64_t n_items = 0, n_fins = 0, n_slots = 0, n_small = 0;
 };
 static std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan> g_plans;
 
@@ -998,7 +1072,10 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   });
   WorkPlan pl;
   pl.n_items = items.size();
+  std::stable_partition(fins.begin(), fins.end(), [](const FinItem& f) { return f.nslots <= kFinSmall; });
   pl.n_fins = fins.size();
+  pl.n_small = static_cast<uint64_t>(
+      std::count_if(fins.begin(), fins.end(), [](const FinItem& f) { return f.nslots <= kFinSmall; }));
   pl.n_slots = static_cast<uint64_t>(slot);
   if (pl.n_items) {
     NTCB_CUDA(cudaMalloc(&pl.d_items, sizeof(WorkItem) * pl.n_items));
@@ -1102,12 +1179,28 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
     else
       launches += launch_items<LD4, NTCB_MAX_ORDER - 1>(ctx, a, pl, smem);
   }
-  if (pl.n_fins) {
-    NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (pl.n_small) {  // warp per row
+    NTCB_CUDA(cudaFuncSetAttribute(k_finalize_small<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
-    const uint64_t fg = std::min<uint64_t>((pl.n_fins + kWarps - 1) / kWarps,
+    UpdateArgs b = a;
+    b.fins = pl.d_fins;
+    b.n_fins = pl.n_small;
+    const uint64_t fg = std::min<uint64_t>((pl.n_small + kWarps - 1) / kWarps,
                                            static_cast<uint64_t>(ctx->sm_count) * 4);
-    k_finalize<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(a);
+    k_finalize_small<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(b);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (pl.n_fins > pl.n_small) {  // CTA per row
+    // warp 0's row-end layout + the per-warp partial sums of one pass
+    const size_t fsmem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
+    NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(fsmem)));
+    UpdateArgs b = a;
+    b.fins = pl.d_fins + pl.n_small;
+    b.n_fins = pl.n_fins - pl.n_small;
+    const uint64_t fg = std::min<uint64_t>(b.n_fins, static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_finalize<LD4><<<static_cast<unsigned>(fg), kWarps * 32, fsmem, ctx->stream>>>(b);
     NTCB_CUDA(cudaGetLastError());
     ++launches;
   }
