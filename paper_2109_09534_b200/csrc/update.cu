@@ -1049,7 +1049,8 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   int64_t slot = 0;
   // Segment length: at most kSeg, and short enough that the range yields ~4
   // items per resident warp (a row shard of a multi-GPU run has few rows).
-  const uint64_t target = 4ull * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps;
+  static const uint64_t ipw = [] { const char* e = std::getenv("NTCB_ITEMS_PER_WARP"); return e ? std::max(1, std::atoi(e)) : 4; }();
+  const uint64_t target = ipw * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps;
   const uint64_t total = off[r1] - off[r0];
   // (small ranges keep whole rows: an extra k_finalize launch costs more there)
   const uint64_t seg = total < (4ull << 20) ? kSeg
