@@ -213,8 +213,14 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
   }
 }
 
+// CUDA-core update CTA shapes: ranks <= 20 -> 8 warps x 2 CTAs (<= 128 regs);
+// 21-32 -> 4 warps x 3 CTAs (<= 170 regs, 12 warps/SM instead of 8);
+// above -> 8 warps x 1 CTA
+__host__ __device__ constexpr int k_update_threads(int LD4) { return (LD4 >= 6 && LD4 <= 8) ? 128 : 256; }
+__host__ __device__ constexpr int k_update_min_blocks(int LD4) { return LD4 <= 5 ? 2 : LD4 <= 8 ? 3 : 1; }
+
 template <int LD4, int NO>
-__global__ void __launch_bounds__(kWarps * 32, (LD4 <= 5 ? 2 : 1)) k_update(UpdateArgs a) {
+__global__ void __launch_bounds__(k_update_threads(LD4), k_update_min_blocks(LD4)) k_update(UpdateArgs a) {
   using W = WarpSmem<LD4>;
   constexpr int L = LD4;          // feature blocks of 4 = lanes (roles) per pick
   constexpr int GP = 32 / L;      // picks per group
@@ -1106,15 +1112,17 @@ void drop_plans(ntcb_context* ctx) {
 
 template <int LD4, int NO>
 static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
+  constexpr int T = k_update_threads(LD4);
+  smem = smem / kWarps * (T / 32);  // per-warp layout
   NTCB_CUDA(cudaFuncSetAttribute(k_update<LD4, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<LD4, NO>, kWarps * 32, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<LD4, NO>, T, smem));
   if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (pl.n_items + kWarps - 1) / kWarps;
+  uint64_t grid = (pl.n_items + T / 32 - 1) / (T / 32);
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   grid = std::max<uint64_t>(grid, 1);
-  k_update<LD4, NO><<<static_cast<unsigned>(grid), kWarps * 32, smem, ctx->stream>>>(a);
+  k_update<LD4, NO><<<static_cast<unsigned>(grid), T, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
   return 1;
 }
