@@ -572,3 +572,42 @@ def test_host_buffers_large_factor_threads(ntc):
         ctx.s_nmc_host(0, bad, a_out, y_out, cfg, 778)
     a2, _ = ctx.get_factor(0)
     np.testing.assert_array_equal(a2, a1)  # rejected before anything was uploaded
+
+
+def test_cfg2_scale_properties(ntc, orc):
+    """BASELINE configs[1] (the bench workload) at full size -- 10^4 x 10^4 x
+    10^4, 10^8 entries: size-independent invariants.  Per-row popcounts of the
+    sampled set equal floor(c n) for every row; 24 rows compared bit-exact with
+    the reference's Fisher-Yates picks; a sweep is deterministic to the bit,
+    accesses sum(b_p), keeps factors nonnegative and lowers the relative error."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [10000, 10000, 10000], 100_000_000, 20
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, nnz, 20, 0.01, 1002)
+    assert ctx.info()[2] == nnz
+    off = ctx.view_offsets(0).astype(np.int64)
+    n = np.diff(off)
+    b = np.floor(0.5 * n.astype(np.float64)).astype(np.int64)
+    st = 0x5EED
+    e0, bits = ctx.sample_mask(0, 0.5, st, 0)
+    assert e0 == 0
+    cnt = np.add.reduceat(bits.astype(np.int64), off[:-1])
+    np.testing.assert_array_equal(cnt, b)
+    rng = np.random.default_rng(5)
+    for p in rng.choice(dims[0], 24, replace=False).tolist():
+        want = np.zeros(int(n[p]), bool)
+        want[orc.sample_row(int(n[p]), 0.5, orc.fork(orc.fork(st, 0), p))] = True
+        np.testing.assert_array_equal(bits[off[p]:off[p + 1]], want)
+    expect = sum(int(np.floor(0.5 * np.diff(ctx.view_offsets(m).astype(np.float64))).sum()) for m in range(3))
+    ctx.random_factors(R, 7)
+    r0 = ctx.relative_error()
+    ctx.sweep_async(0, P.NmcConfig(c=0.5), 7)
+    assert ctx.collect() == expect
+    A1 = [ctx.get_factor(m)[0] for m in range(3)]
+    assert ctx.relative_error() < r0
+    assert all(np.all(a >= 0) for a in A1)
+    ctx.random_factors(R, 7)
+    ctx.sweep_async(0, P.NmcConfig(c=0.5), 7)
+    ctx.collect()
+    for m in range(3):
+        np.testing.assert_array_equal(ctx.get_factor(m)[0], A1[m])
