@@ -163,17 +163,25 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
   for (int r = lane; r < R; r += 32) vv[r] = v0;
   __syncwarp();
   double rq = 0.0, rq_prev = 0.0;
+  // (H + lambda I) v with four partial sums per row: the iteration is a
+  // latency chain (mat-vec -> two warp reductions -> normalise), and short
+  // rows are dominated by it
+  auto hrow_dot = [&](int r) {
+    const float* hr = Hf + r * HS;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = 0;
+    for (; j + 4 <= R; j += 4) {
+      s0 += static_cast<double>(hr[j]) * vv[j];
+      s1 += static_cast<double>(hr[j + 1]) * vv[j + 1];
+      s2 += static_cast<double>(hr[j + 2]) * vv[j + 2];
+      s3 += static_cast<double>(hr[j + 3]) * vv[j + 3];
+    }
+    for (; j < R; ++j) s0 += static_cast<double>(hr[j]) * vv[j];
+    return ((s0 + s1) + (s2 + s3)) + lam * vv[r];
+  };
   for (int it = 0; it < a.power_iters; ++it) {
-    double u0 = 0.0, u1 = 0.0;
-    if (lane < R) {
-      const float* hr = Hf + lane * HS;
-      for (int j = 0; j < R; ++j) u0 += (static_cast<double>(hr[j]) + (j == lane ? lam : 0.0)) * vv[j];
-    }
-    if (lane + 32 < R) {
-      const float* hr = Hf + (lane + 32) * HS;
-      for (int j = 0; j < R; ++j)
-        u1 += (static_cast<double>(hr[j]) + (j == lane + 32 ? lam : 0.0)) * vv[j];
-    }
+    const double u0 = lane < R ? hrow_dot(lane) : 0.0;
+    const double u1 = lane + 32 < R ? hrow_dot(lane + 32) : 0.0;
     double num = 0.0, un2 = u0 * u0 + u1 * u1;
     if (lane < R) num += vv[lane] * u0;
     if (lane + 32 < R) num += vv[lane + 32] * u1;
