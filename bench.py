@@ -388,7 +388,7 @@ def run_ours(args, cfgd, cid):
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_update (gradient+Hessian+power method+step)",
                          "alg_bytes_per_launch": per_launch_bytes,
-                         "avg_launch_ms": avg_upd_s * 1000.0,
+                         "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)
                          "sampler_ms_per_step": smp_ms / args.steps,
                          "update_ms_per_step": upd_ms / args.steps,
                          "compute": compute, "limiter": limiter},

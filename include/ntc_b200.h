@@ -231,9 +231,11 @@ int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                int value_kind);
 
 /* ---- timing hooks for bench.py ----------------------------------------- */
-/* Kernel-level timing of the last ntcb_collect window: total device ms of
- * the update (accumulate) kernels and of the sampler kernels, and number of
- * kernel launches, measured with CUDA events on the context stream. */
+/* Kernel-level timing since profiling was enabled (or the last read): total
+ * device ms of the timed mode updates (update kernel + split-row
+ * finalisation, CUDA events on the context stream) and of the sampler phases
+ * (side stream), the number of kernel launches issued, and the number of
+ * timed mode updates (update_launches; at most 2048 phases are timed). */
 int ntcb_profile_enable(ntcb_context* ctx, int on);
 int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms,
                       uint64_t* launches, uint64_t* update_launches);

@@ -993,18 +993,21 @@ int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms, u
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   Profile& pf = ctx->prof;
   double u = 0.0, s = 0.0;
+  uint64_t nu = 0;
   for (int i = 0; i + 1 < pf.n; i += 2) {
     float ms = 0.f;
     NTCB_CUDA(cudaEventElapsedTime(&ms, pf.ev[i], pf.ev[i + 1]));
-    if (pf.kind[i / 2] == 0)
+    if (pf.kind[i / 2] == 0) {
       u += ms;
-    else
+      ++nu;
+    } else {
       s += ms;
+    }
   }
   if (update_ms) *update_ms = u;
   if (sample_ms) *sample_ms = s;
   if (launches) *launches = pf.launches;
-  if (update_launches) *update_launches = pf.update_launches;
+  if (update_launches) *update_launches = nu;
   pf.n = 0;
   pf.launches = 0;
   pf.update_launches = 0;
