@@ -56,6 +56,7 @@ struct HostState {
   std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, uint64_t> bs_cache;
   float* stage = nullptr;  // pinned fp32 staging for host-buffer factor transfers
   uint64_t stage_n = 0;    // floats
+  bool queued = false;     // work enqueued since the last collect
 };
 std::map<const ntcb_context*, HostState> g_host;
 
@@ -177,23 +178,29 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
     NTCB_CUDA(cudaEventRecord(ctx->ev_consumed[mode][par], st));
     ctx->consumed_valid[mode][par] = true;
   }
+  g_host[ctx].queued = true;
   g_host[ctx].pending_accessed +=
       static_cast<uint64_t>(cfg.max_inner) * blocksize_sum(ctx, mode, r0, r1, cfg.c);
 }
 
 // Waits and converts a device-side row failure into the reference's exception.
+// One host synchronisation: the main stream waits for the side stream, then
+// the error key comes back by an async copy into pinned memory.
 void collect(ntcb_context* ctx, uint64_t* accessed) {
-  NTCB_CUDA(cudaStreamSynchronize(ctx->side));
+  NTCB_CUDA(cudaEventRecord(ctx->ev_side_done, ctx->side));
+  NTCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_side_done, 0));
+  NTCB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, ctx->stream));
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
-  NTCB_CUDA(cudaMemcpy(ctx->h_counters, ctx->counters, 2 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost));
   auto& hs = g_host[ctx];
+  hs.queued = false;
   const unsigned long long key = ctx->h_counters[1];
   const uint64_t pend = hs.pending_accessed;
   hs.pending_accessed = 0;
   if (key != ~0ull) {
     const unsigned long long reset = ~0ull;
-    NTCB_CUDA(cudaMemcpy(ctx->counters + 1, &reset, sizeof reset, cudaMemcpyHostToDevice));
+    NTCB_CUDA(cudaMemcpyAsync(ctx->counters + 1, &reset, sizeof reset, cudaMemcpyHostToDevice, ctx->stream));
+    NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
     const int mode = static_cast<int>(key >> 58);
     const uint64_t row = (key >> 2) & ((1ull << 56) - 1);
     const int kind = static_cast<int>(key & 3);
@@ -320,13 +327,18 @@ bool upload_factor_async(ntcb_context* ctx, float* dst, const double* src, uint6
   return true;
 }
 
-// A and/or Y of `mode` -> pinned staging (one sync) -> host doubles
-void download_factors(ntcb_context* ctx, int mode, double* a, double* y) {
-  const uint64_t R = ctx->rank, ld = ctx->ld, rows = ctx->dims[mode], n = rows * ld;
+// A and/or Y of `mode` -> pinned staging (async on the main stream)
+void download_factors_enqueue(ntcb_context* ctx, int mode, bool a, bool y) {
+  const uint64_t ld = ctx->ld, rows = ctx->dims[mode], n = rows * ld;
   float* tmp = host_stage(ctx, 2 * n);
   if (a) NTCB_CUDA(cudaMemcpyAsync(tmp, ctx->A[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
   if (y) NTCB_CUDA(cudaMemcpyAsync(tmp + n, ctx->Y[mode], sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
-  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// staging -> host doubles (after the main stream has been synchronised)
+void download_factors_finish(ntcb_context* ctx, int mode, double* a, double* y) {
+  const uint64_t R = ctx->rank, ld = ctx->ld, rows = ctx->dims[mode], n = rows * ld;
+  float* tmp = g_host[ctx].stage;
   parallel_rows(rows, 2 * R, [&](uint64_t i0, uint64_t i1) {
     for (int w = 0; w < 2; ++w) {
       double* dst = w ? y : a;
@@ -337,6 +349,13 @@ void download_factors(ntcb_context* ctx, int mode, double* a, double* y) {
     }
     return true;
   });
+}
+
+// A and/or Y of `mode` -> host doubles (one synchronisation)
+void download_factors(ntcb_context* ctx, int mode, double* a, double* y) {
+  download_factors_enqueue(ctx, mode, a != nullptr, y != nullptr);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  download_factors_finish(ctx, mode, a, y);
 }
 
 void upload_factor(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
@@ -437,6 +456,7 @@ int ntcb_create(int device, ntcb_context** out) {
     for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& mm : ctx->ev_consumed)
     for (auto& e : mm) NTCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NTCB_CUDA(cudaEventCreateWithFlags(&ctx->ev_side_done, cudaEventDisableTiming));
   NTCB_CUDA(cudaMalloc(&ctx->counters, 8 * sizeof(unsigned long long)));
   NTCB_CUDA(cudaMallocHost(&ctx->h_counters, 8 * sizeof(unsigned long long)));
   const unsigned long long init[8] = {0, ~0ull, 0, 0, 0, 0, 0, 0};
@@ -462,6 +482,7 @@ int ntcb_destroy(ntcb_context* ctx) {
     for (auto& e : mm) cudaEventDestroy(e);
   for (auto& mm : ctx->ev_consumed)
     for (auto& e : mm) cudaEventDestroy(e);
+  if (ctx->ev_side_done) cudaEventDestroy(ctx->ev_side_done);
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
   if (g_host[ctx].stage) cudaFreeHost(g_host[ctx].stage);
@@ -704,8 +725,10 @@ int ntcb_factor_device_ptr(ntcb_context* ctx, int mode, int which, void** ptr, u
   API_CATCH
 }
 
-int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc_config* cfg,
-               uint64_t rng_state, uint64_t* entries_accessed) {
+// ntcb_s_nmc / ntcb_s_nmc_host: the host-buffer form enqueues the copies of
+// the updated factor and momentum before the call's single synchronisation
+static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double* a_out, double* y_out,
+                      bool outs, const ntcb_nmc_config* cfg, uint64_t rng_state, uint64_t* entries_accessed) {
   API_TRY
   need_ctx(ctx);
   validate_nmc(cfg);
@@ -713,7 +736,7 @@ int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
   auto& hs = g_host[ctx];
   if (!a_init && !hs.verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
-  collect(ctx, nullptr);  // drain anything queued before
+  if (hs.queued) collect(ctx, nullptr);  // drain (and report) anything queued before
   int pre = -1;
   if (a_init) {
     // the first sample does not read factors: it runs on the side stream
@@ -727,16 +750,21 @@ int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc
     hs.verified[mode] = true;
   }
   enqueue_snmc(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, pre);
-  collect(ctx, entries_accessed);
+  if (outs) download_factors_enqueue(ctx, mode, a_out != nullptr, y_out != nullptr);
+  collect(ctx, entries_accessed);  // the one synchronisation of the call
+  if (outs) download_factors_finish(ctx, mode, a_out, y_out);
   API_CATCH
+}
+
+int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc_config* cfg,
+               uint64_t rng_state, uint64_t* entries_accessed) {
+  return s_nmc_impl(ctx, mode, a_init, nullptr, nullptr, false, cfg, rng_state, entries_accessed);
 }
 
 int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a_out,
                     double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
                     uint64_t* entries_accessed) {
-  int rc = ntcb_s_nmc(ctx, mode, a_init, cfg, rng_state, entries_accessed);
-  if (rc) return rc;
-  return ntcb_factor_get(ctx, mode, a_out, y_out);
+  return s_nmc_impl(ctx, mode, a_init, a_out, y_out, true, cfg, rng_state, entries_accessed);
 }
 
 int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,

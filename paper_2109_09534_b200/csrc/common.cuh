@@ -120,6 +120,7 @@ struct ntcb_context {
   cudaStream_t side = nullptr;  // sampler stream (sampling never reads factors)
   cudaEvent_t ev_sampled[NTCB_MAX_ORDER][2] = {};
   cudaEvent_t ev_consumed[NTCB_MAX_ORDER][2] = {};
+  cudaEvent_t ev_side_done = nullptr;  // collect(): the main stream waits for the side stream
   bool consumed_valid[NTCB_MAX_ORDER][2] = {};
   float* partial = nullptr;  // split-row partial sums
   uint64_t partial_n = 0;
