@@ -173,11 +173,13 @@ void radix_pairs(ntcb_context* ctx, KT* keys, KT* keys_alt, uint32_t* vals, uint
 void drop_plans(ntcb_context* ctx);
 void drop_heavy(ntcb_context* ctx);
 void drop_sample_plans(ntcb_context* ctx);
+void drop_metric_plans(ntcb_context* ctx);
 
 void free_views(ntcb_context* ctx) {
   drop_plans(ctx);
   drop_heavy(ctx);
   drop_sample_plans(ctx);
+  drop_metric_plans(ctx);
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
     DeviceView& v = ctx->views[m];
     if (v.off) cudaFree(v.off);
