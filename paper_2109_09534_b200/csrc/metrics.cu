@@ -193,10 +193,14 @@ const MPlan& mplan(ntcb_context* ctx) {
   const DeviceView& v = ctx->views[0];
   auto it = g_mplans.find(v.off);
   if (it != g_mplans.end()) return it->second;
+  // items of <= kItem entries, shorter when the tensor is small (~2 per warp slot)
+  const uint64_t nnz = v.h_off[v.rows];
+  const uint64_t slots = static_cast<uint64_t>(ctx->sm_count) * 32;
+  const uint64_t len = std::min<uint64_t>(kItem, std::max<uint64_t>(256, (nnz / (2 * slots) + 31) / 32 * 32));
   std::vector<MItem> items;
   for (uint64_t p = 0; p < v.rows; ++p)
-    for (uint64_t e = v.h_off[p]; e < v.h_off[p + 1]; e += kItem)
-      items.push_back({p, e, std::min<uint64_t>(v.h_off[p + 1], e + kItem)});
+    for (uint64_t e = v.h_off[p]; e < v.h_off[p + 1]; e += len)
+      items.push_back({p, e, std::min<uint64_t>(v.h_off[p + 1], e + len)});
   MPlan pl;
   pl.n = items.size();
   if (pl.n) {
