@@ -49,6 +49,8 @@ struct Buf {
 struct Dims {
   uint64_t d[NTCB_MAX_ORDER];
   int shift[NTCB_MAX_ORDER];
+  uint64_t stride[NTCB_MAX_ORDER];  // mixed-radix linear key when the bit-packed one exceeds 64 bits
+  int linear;
   const double* cdf[NTCB_MAX_ORDER];     // Zipf modes: CDF over ranks (nullptr = uniform)
   const uint32_t* perm[NTCB_MAX_ORDER];  // Zipf modes: rank -> id
   int order;
@@ -74,7 +76,10 @@ __global__ void k_candidates(uint64_t s_mask, uint64_t M, Dims d, uint64_t* key,
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < M;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t k = 0;
-    for (int m = 0; m < d.order; ++m) k |= static_cast<uint64_t>(coord_of(d, s_mask, j, m)) << d.shift[m];
+    if (d.linear)
+      for (int m = 0; m < d.order; ++m) k += static_cast<uint64_t>(coord_of(d, s_mask, j, m)) * d.stride[m];
+    else
+      for (int m = 0; m < d.order; ++m) k |= static_cast<uint64_t>(coord_of(d, s_mask, j, m)) << d.shift[m];
     key[j] = k;
     jj[j] = static_cast<uint32_t>(j);
   }
@@ -184,7 +189,17 @@ void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
     bits += b;
     cells *= static_cast<long double>(dims[m]);
   }
-  if (bits > 64) fail(NTCB_EINVAL, "synth: packed cell key exceeds 64 bits");
+  if (bits > 64) {
+    // the cell id as a mixed-radix number (4.8M x 1.8M x 1.8M = 1.6e19 < 2^64)
+    if (cells >= 18446744073709551615.0L) fail(NTCB_EINVAL, "synth: cell space exceeds 2^64");
+    d.linear = 1;
+    uint64_t st = 1;
+    for (int m = order - 1; m >= 0; --m) {
+      d.stride[m] = st;
+      st *= dims[m];
+    }
+    bits = 64;
+  }
   if (static_cast<long double>(nnz) > 0.5L * cells)
     fail(NTCB_EINVAL, "synth: nnz exceeds half the cell space");
   if (true_rank == 0 || true_rank > 256) fail(NTCB_EINVAL, "synth: bad true rank");
