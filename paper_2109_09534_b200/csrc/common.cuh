@@ -70,7 +70,6 @@ struct DeviceView {
   uint32_t* oth[NTCB_MAX_ORDER - 1] = {};
   float* val = nullptr;
   uint64_t* h_off = nullptr;  // host copy of the offsets (shard planning, blocksizes)
-  uint64_t light_cap = 0;     // sampler: slices up to this length use shared memory
 };
 
 // Kernel-argument bundle describing the factor matrices.

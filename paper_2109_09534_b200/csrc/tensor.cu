@@ -305,24 +305,8 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
                               cudaMemcpyDeviceToHost, st));
     NTCB_CUDA(cudaStreamSynchronize(st));
     uint64_t mx = 0;
-    std::vector<uint64_t> lens;
-    lens.reserve(v.rows);
-    for (uint64_t p = 0; p < v.rows; ++p) {
-      const uint64_t n = v.h_off[p + 1] - v.h_off[p];
-      mx = std::max(mx, n);
-      if (n > 1) lens.push_back(n);
-    }
+    for (uint64_t p = 0; p < v.rows; ++p) mx = std::max(mx, v.h_off[p + 1] - v.h_off[p]);
     v.max_slice = mx;
-    // Sampler shared-memory cap (CTA kernel, 4 bytes per entry): twice the 99th
-    // percentile slice (>= 2048, <= 49152 entries); only the longer tail goes to
-    // the grid path, so a few Zipf-heavy slices do not shrink every CTA's occupancy.
-    uint64_t cap = std::min<uint64_t>(mx, 49152);
-    if (lens.size() > 100) {
-      const size_t q = lens.size() - 1 - lens.size() / 100;
-      std::nth_element(lens.begin(), lens.begin() + q, lens.end());
-      cap = std::min<uint64_t>(cap, std::max<uint64_t>(2 * lens[q], 2048));
-    }
-    v.light_cap = (cap + 255) / 256 * 256;
   }
   ctx->mask_words = nnz / 32 + 2;
   for (int m = 0; m < order; ++m)
