@@ -291,13 +291,15 @@ def run_ours(args, cfgd, cid):
                "achieved_tflops": flops_launch / avg_upd_s / 1e12,
                "fp32_peak_tflops": fp32_peak, "fp32_peak_source": "measured FFMA, tools/microbench/hmma.cu",
                "frac_fp32": flops_launch / avg_upd_s / 1e12 / fp32_peak}
-    limiter = ("L1/LSU data pipe: two factor-row gathers from L2 per sampled nnz (ncu: LSU wavefronts "
-               "80% of peak, DRAM 11%; profiles/r01_v9_k_update_tc.txt); Gram on tensor cores")
+    limiter = {"unit": "L1/LSU data pipe (two factor-row gathers from L2 per sampled nnz; Gram on tensor cores)",
+               "util": None, "dram_util": None, "source": None}
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        limiter.update({k: tj.get(k) for k in ("util", "dram_util", "source") if k in tj})
 
     # ---- end to end through the host-buffer C-ABI --------------------------------
     e2e = None
@@ -386,10 +388,11 @@ def run_ours(args, cfgd, cid):
             "sec_per_ao_iteration": ms / args.steps / 1000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_update (gradient+Hessian+power method+step)",
+                         "kernel": "k_update_tc (gradient + tensor-core Hessian + power method + step)",
                          "alg_bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)
-                         "sampler_ms_per_step": smp_ms / args.steps,
+                         # side-stream spans include queueing behind the update: not busy time
+                         "sampler_span_ms_per_step": smp_ms / args.steps,
                          "update_ms_per_step": upd_ms / args.steps,
                          "compute": compute, "limiter": limiter},
             "clocks": clocks, "gpu_launches": launches,
