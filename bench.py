@@ -388,7 +388,9 @@ def run_ours(args, cfgd, cid):
             "sec_per_ao_iteration": ms / args.steps / 1000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_update_tc (gradient + tensor-core Hessian + power method + step)",
+                         "kernel": ("k_update_tc (gradient + tensor-core Hessian + power method + step)"
+                                    if R <= 31 and order <= 4 else
+                                    "k_update (gradient + CUDA-core Hessian + power method + step)"),
                          "alg_bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)
                          # side-stream spans include queueing behind the update: not busy time
