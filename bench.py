@@ -357,8 +357,9 @@ def run_ours(args, cfgd, cid):
         e_ms = float(t.item())
         e2e = {"value": full * args.steps / (e_ms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "per mode: shard a_init rows pinned host -> device, sharded S_NMC + "
-                       "NCCL all-gather, full factor device -> pinned host (rank-local bytes)"}
+               "path": f"per mode: shard a_init rows pinned host -> device, sharded S_NMC + "
+                       f"{'fused peer-store exchange + NCCL barrier' if sharded.p2p else 'NCCL all-gather'}, "
+                       f"full factor device -> pinned host (rank-local bytes)"}
 
     # ---- CPU baseline: the reference on this box's cores (rank 0, N=1) -----------
     cpu = None
@@ -381,6 +382,7 @@ def run_ours(args, cfgd, cid):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded device generator; BASELINE configs shape)",
             "config": {"workload": workload_name(cid, cfgd), "dims": dims, "nnz": cfgd["nnz"],
+                       "exchange": (sharded.exchange if sharded else "none"),
                        "rank": R, "c": 0.5, "max_inner": 1, "lambda": 1e-3,
                        "sampled_per_ao_iteration": full,
                        "l2": "inputs larger than L2: views stream 12 B/entry x 100M per mode per iteration",

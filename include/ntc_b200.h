@@ -154,6 +154,23 @@ int ntcb_factor_get(ntcb_context* ctx, int mode, double* a, double* y);
  * dims[mode] rows, row stride *ld floats (ld >= rank, padding is zero). */
 int ntcb_factor_device_ptr(ntcb_context* ctx, int mode, int which, void** ptr, uint64_t* ld);
 
+/* ---- fused exchange for row-sharded multi-GPU runs -----------------------
+ * Replicas of factor A[mode] on other GPUs (same dims, same ld) can be
+ * registered as peers: every row an S_NMC call finalises is then also
+ * stored into each peer replica by the update kernel itself (NVLink P2P
+ * stores, issued row by row while other rows are still computing), so a
+ * row-sharded sweep needs only a barrier after each mode instead of an
+ * all-gather.  The peers see the rows once this call's kernels completed
+ * and a cross-GPU barrier ordered after them (e.g. a one-element NCCL
+ * all-reduce on the library stream) returned.
+ * ntcb_factor_ipc_handle: the CUDA IPC handle (64 bytes) of A[mode];
+ * ntcb_ipc_open: maps another process's handle into this one (lazy peer
+ * access); ntcb_factor_set_peers: registers n <= 7 device pointers to peer
+ * replicas of A[mode] (n = 0 clears). */
+int ntcb_factor_ipc_handle(ntcb_context* ctx, int mode, void* handle64);
+int ntcb_ipc_open(ntcb_context* ctx, const void* handle64, void** ptr);
+int ntcb_factor_set_peers(ntcb_context* ctx, int mode, int n, void* const* peer_ptrs);
+
 /* ---- S_NMC (nmc.hpp:93-95, nmc.cpp:199-272) -----------------------------
  * One call = one ntc::s_nmc(views[mode], factors, mode, a_init, cfg,
  * RngStream(rng_state), &stats): A = Y = a_init, then max_inner inner

@@ -96,6 +96,9 @@ SIGNATURES = {
     "ntcb_factor_get": (C.c_int, [C.c_void_p, C.c_int, f64p, f64p]),
     "ntcb_factor_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p),
                                          u64p]),
+    "ntcb_factor_ipc_handle": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ntcb_ipc_open": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ntcb_factor_set_peers": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ntcb_s_nmc": (C.c_int, [C.c_void_p, C.c_int, f64p, C.POINTER(NmcConfigC), C.c_uint64, u64p]),
     "ntcb_s_nmc_host": (C.c_int, [C.c_void_p, C.c_int, f64p, f64p, f64p, C.POINTER(NmcConfigC),
                                   C.c_uint64, u64p]),

@@ -391,6 +391,7 @@ void free_factors(ntcb_context* ctx) {
     ctx->A[m] = ctx->Y[m] = nullptr;
   }
   ctx->rank = ctx->ld = 0;
+  for (int m = 0; m < NTCB_MAX_ORDER; ++m) ctx->n_peers[m] = 0;
 }
 
 void alloc_factors(ntcb_context* ctx, uint64_t rank) {
@@ -486,6 +487,7 @@ int ntcb_destroy(ntcb_context* ctx) {
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
   if (g_host[ctx].stage) cudaFreeHost(g_host[ctx].stage);
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   g_host.erase(ctx);
   delete ctx;
   API_CATCH
@@ -712,6 +714,46 @@ int ntcb_factor_get(ntcb_context* ctx, int mode, double* a, double* y) {
   need_factors(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_get: mode out of range");
   download_factors(ctx, mode, a, y);
+  API_CATCH
+}
+
+int ntcb_factor_ipc_handle(ntcb_context* ctx, int mode, void* handle64) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_ipc_handle: mode out of range");
+  if (!handle64) fail(NTCB_EINVAL, "factor_ipc_handle: null output");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+  cudaIpcMemHandle_t h;
+  NTCB_CUDA(cudaIpcGetMemHandle(&h, ctx->A[mode]));
+  std::memcpy(handle64, &h, sizeof h);
+  API_CATCH
+}
+
+int ntcb_ipc_open(ntcb_context* ctx, const void* handle64, void** ptr) {
+  API_TRY
+  need_ctx(ctx);
+  if (!handle64 || !ptr) fail(NTCB_EINVAL, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  void* p = nullptr;
+  NTCB_CUDA(cudaSetDevice(ctx->device));
+  NTCB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ctx->ipc_opened.push_back(p);
+  *ptr = p;
+  API_CATCH
+}
+
+int ntcb_factor_set_peers(ntcb_context* ctx, int mode, int n, void* const* peer_ptrs) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_set_peers: mode out of range");
+  if (n < 0 || n > 7) fail(NTCB_EINVAL, "factor_set_peers: at most 7 peers");
+  if (n > 0 && !peer_ptrs) fail(NTCB_EINVAL, "factor_set_peers: null pointer array");
+  collect(ctx, nullptr);  // no queued update may still use the old peer set
+  for (int q = 0; q < 7; ++q) ctx->peerA[mode][q] = q < n ? static_cast<float*>(peer_ptrs[q]) : nullptr;
+  ctx->n_peers[mode] = n;
   API_CATCH
 }
 

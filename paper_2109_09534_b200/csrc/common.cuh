@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <vector>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -110,6 +112,9 @@ struct ntcb_context {
   uint64_t rank = 0;
   uint64_t ld = 0;
   float* A[NTCB_MAX_ORDER] = {};
+  float* peerA[NTCB_MAX_ORDER][7] = {};  // replicas of A[m] on other GPUs (fused exchange)
+  int n_peers[NTCB_MAX_ORDER] = {};
+  std::vector<void*> ipc_opened;          // mappings to close at destroy
   float* Y[NTCB_MAX_ORDER] = {};
 
   // sampled-set masks, one bit per view entry, per (mode, inner-iteration parity)

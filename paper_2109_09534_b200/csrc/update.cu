@@ -65,6 +65,8 @@ struct UpdateArgs {
   int ld;                              // factor row stride (floats)
   float* A;
   float* Y;
+  float* peerA[7];  // replicas of A on other GPUs: finalised rows are stored there too
+  int n_peers;
   const WorkItem* items;
   uint64_t n_items;
   const FinItem* fins;
@@ -218,7 +220,11 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
     const double an = av > 0.0 ? av : 0.0;
     a.A[p * ld + r] = static_cast<float>(an);
     a.Y[p * ld + r] = static_cast<float>(an + beta * (an - ap));
+    // the fused exchange: the row goes to every peer replica over NVLink now,
+    // overlapped with the rows still being computed (no all-gather after)
+    for (int q = 0; q < a.n_peers; ++q) a.peerA[q][p * ld + r] = static_cast<float>(an);
   }
+  if (a.n_peers) __threadfence_system();
 }
 
 // CUDA-core update CTA shapes: ranks <= 20 -> 8 warps x 2 CTAs (<= 128 regs);
@@ -1256,6 +1262,8 @@ int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_
   a.ld = static_cast<int>(ctx->ld);
   a.A = ctx->A[mode];
   a.Y = ctx->Y[mode];
+  a.n_peers = ctx->n_peers[mode];
+  for (int q = 0; q < 7; ++q) a.peerA[q] = ctx->peerA[mode][q];
   a.items = pl.d_items;
   a.n_items = pl.n_items;
   a.fins = pl.d_fins;

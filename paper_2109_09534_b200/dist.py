@@ -103,33 +103,87 @@ def factor_tensor(ctx, mode: int, rows: int, which: int = 0):
     return torch.as_tensor(_CudaArray(ptr, (rows, ld)), device=f"cuda:{ctx.device}")
 
 
-class ShardedSweep:
-    """Drives ntcb over this rank's row shard of every mode, then all-gathers."""
+def setup_p2p(ctx, rank: int, world: int, group=None) -> bool:
+    """Fused exchange: every rank maps every other rank's factor replicas (CUDA
+    IPC, lazy peer access) and registers them with its context, so the update
+    kernel stores each finalised row into all replicas itself.  Collective:
+    every rank must call it.  Returns False (nothing registered) when any rank
+    cannot map a peer, so all ranks fall back to the all-gather together."""
+    import torch.distributed as tdist
+    order = ctx.info()[0]
+    handles = [ctx.factor_ipc_handle(m) for m in range(order)]
+    allh = [None] * world
+    tdist.all_gather_object(allh, handles, group=group)
+    ok, ptrs = True, [[] for _ in range(order)]
+    try:
+        for k in range(world):
+            if k == rank:
+                continue
+            for m in range(order):
+                ptrs[m].append(ctx.ipc_open(allh[k][m]))
+    except Exception:
+        ok = False
+    flags = [None] * world
+    tdist.all_gather_object(flags, ok, group=group)
+    if not all(flags):
+        return False
+    for m in range(order):
+        ctx.set_factor_peers(m, ptrs[m])
+    return True
 
-    def __init__(self, ctx, cfg, rank: int, world: int, group=None):
+
+class ShardedSweep:
+    """Drives ntcb over this rank's row shard of every mode, then exchanges
+    the updated factor: by the update kernel's own peer stores plus a barrier
+    (exchange="p2p", the default when every GPU can map every other's
+    memory) or by an NCCL all-gather of the shards (exchange="gather")."""
+
+    def __init__(self, ctx, cfg, rank: int, world: int, group=None, exchange: str = "auto"):
+        import os
+
         import torch
+        import torch.distributed as tdist
         self.ctx, self.cfg, self.rank, self.world, self.group = ctx, cfg, rank, world, group
         order, dims, _ = ctx.info()
         self.dims = dims
         self.bounds = [partition_rows(ctx.view_offsets(m), cfg.c, world) for m in range(order)]
         self.A = [factor_tensor(ctx, m, dims[m]) for m in range(order)]
-        import torch.distributed as tdist
-        # the exchange runs whenever a process group exists (at world size 1 too:
-        # NTCB_FORCE_SHARDED exercises the NCCL path on one GPU)
-        self.gather = [RowGather(self.A[m], self.bounds[m], rank, group) for m in range(order)] \
-            if tdist.is_available() and tdist.is_initialized() else None
         st = torch.cuda.current_stream()
         if st.cuda_stream == 0:  # legacy default stream has no handle; use a real one
             st = torch.cuda.Stream()
             torch.cuda.set_stream(st)
         ctx.set_stream(st.cuda_stream)
+        dist_on = tdist.is_available() and tdist.is_initialized()
+        if exchange == "auto":
+            exchange = os.environ.get("NTCB_EXCHANGE", "p2p")
+        self.p2p = bool(dist_on and world > 1 and exchange == "p2p" and setup_p2p(ctx, rank, world, group))
+        self.exchange = "p2p" if self.p2p else "gather"
+        # the exchange runs whenever a process group exists (at world size 1 too:
+        # NTCB_FORCE_SHARDED exercises the NCCL path on one GPU)
+        self.gather = None if (self.p2p or not dist_on) else \
+            [RowGather(self.A[m], self.bounds[m], rank, group) for m in range(order)]
+        self.nccl = dist_on and tdist.get_backend(group) == "nccl"
+        self.flag = torch.zeros(1, dtype=torch.int32, device="cuda" if self.nccl else "cpu")
+
+    def barrier(self) -> None:
+        """Every rank's queued updates (and their peer stores) are complete
+        before anything this rank enqueues next: a one-element NCCL all-reduce
+        ordered on the stream, or collect + a host barrier on gloo."""
+        import torch.distributed as tdist
+        if self.nccl:
+            tdist.all_reduce(self.flag, group=self.group)
+        else:
+            self.ctx.collect()
+            tdist.barrier(group=self.group)
 
     def sweep_mode(self, k: int, m: int, seed: int) -> None:
         """This rank's rows of the mode-m update of sweep k, then the exchange."""
         from .ntc import sweep_stream
         r0, r1 = self.bounds[m][self.rank]
         self.ctx.s_nmc_rows_async(m, r0, r1, self.cfg, sweep_stream(seed, k, m).state)
-        if self.gather is not None:
+        if self.p2p:
+            self.barrier()
+        elif self.gather is not None:
             self.gather[m]()
 
     def sweep(self, k: int, seed: int) -> None:

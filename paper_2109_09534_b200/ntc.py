@@ -308,6 +308,22 @@ class Context:
         check(self.L.ntcb_factor_device_ptr(self.h, mode, which, C.byref(p), C.byref(ld)))
         return p.value, ld.value
 
+    # fused exchange (row-sharded multi-GPU) ------------------------------
+    def factor_ipc_handle(self, mode) -> bytes:
+        buf = (C.c_ubyte * 64)()
+        check(self.L.ntcb_factor_ipc_handle(self.h, mode, buf))
+        return bytes(buf)
+
+    def ipc_open(self, handle: bytes) -> int:
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        p = C.c_void_p()
+        check(self.L.ntcb_ipc_open(self.h, buf, C.byref(p)))
+        return p.value
+
+    def set_factor_peers(self, mode, ptrs):
+        arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+        check(self.L.ntcb_factor_set_peers(self.h, mode, len(ptrs), arr))
+
     # solver -------------------------------------------------------------
     def s_nmc(self, mode, cfg: NmcConfig, rng_state: int, a_init=None) -> int:
         acc = C.c_uint64(0)
