@@ -490,8 +490,8 @@ def test_read_write_tns_device(ntc, tmp_path, golden):
     np.testing.assert_array_equal(c.canonical()[0], golden["t1_canon_idx"])
 
 
-@pytest.mark.parametrize("order,R", [(2, 1), (2, 7), (3, 1), (3, 4), (3, 13), (3, 32), (3, 41),
-                                     (3, 64), (4, 16), (5, 6), (6, 9)])
+@pytest.mark.parametrize("order,R", [(2, 1), (2, 7), (3, 1), (3, 4), (3, 13), (3, 20), (3, 27), (3, 32),
+                                     (3, 41), (3, 64), (4, 16), (4, 24), (4, 32), (5, 6), (6, 9)])
 def test_ranks_and_orders_vs_oracle(ntc, orc, order, R):
     """Every kernel instantiation class: L = ceil(R/4) from 1 to 16 (incl. the
     register-spilling large-R ones), orders 2..6 (the generic-order path);
