@@ -111,18 +111,23 @@ def setup_p2p(ctx, rank: int, world: int, group=None) -> bool:
     cannot map a peer, so all ranks fall back to the all-gather together."""
     import torch.distributed as tdist
     order = ctx.info()[0]
-    handles = [ctx.factor_ipc_handle(m) for m in range(order)]
+    # every rank reaches every collective below, whatever fails locally
+    try:
+        handles = [ctx.factor_ipc_handle(m) for m in range(order)]
+    except Exception:
+        handles = None
     allh = [None] * world
     tdist.all_gather_object(allh, handles, group=group)
-    ok, ptrs = True, [[] for _ in range(order)]
-    try:
-        for k in range(world):
-            if k == rank:
-                continue
-            for m in range(order):
-                ptrs[m].append(ctx.ipc_open(allh[k][m]))
-    except Exception:
-        ok = False
+    ok, ptrs = all(h is not None for h in allh), [[] for _ in range(order)]
+    if ok:
+        try:
+            for k in range(world):
+                if k == rank:
+                    continue
+                for m in range(order):
+                    ptrs[m].append(ctx.ipc_open(allh[k][m]))
+        except Exception:
+            ok = False
     flags = [None] * world
     tdist.all_gather_object(flags, ok, group=group)
     if not all(flags):
