@@ -32,6 +32,7 @@
 #include <cstring>
 #include <map>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -616,8 +617,10 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
   return WarpSmem<1>::stage_words(no) > WarpSmem<1>::ktile_words(R) + 256 ? WarpSmem<1>::stage_words(no)
                                                                           : WarpSmem<1>::ktile_words(R) + 256;
 }
-__host__ __device__ constexpr int tc_words(int no, int R) {
-  return tc_ring_words(no, R) + WarpSmem<1>::batch_words(no);
+constexpr int kKtStride = 36;          // natural layout: k' tile row stride (floats, bank-skewed)
+constexpr int kKtWords = 8 * kKtStride;  // 8 picks
+__host__ __device__ constexpr int tc_words(int no, int R, bool nat = false) {
+  return tc_ring_words(no, R) + WarpSmem<1>::batch_words(no) + (nat ? kKtWords : 0);
 }
 
 // base + row * ld4 bytes as one wide multiply-add
@@ -627,7 +630,13 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
   return reinterpret_cast<const float*>(p);
 }
 
-template <int P, int NO>
+// NAT (natural gather, ranks 25-32 at ld = 32): a pick's row of each other
+// factor is one 128-byte line read by 8 consecutive lanes as float4 (one
+// wavefront per row and mode instead of the pair layout's ~3); the
+// Khatri-Rao rows k go through an 8 x 32 shared tile into the fragment
+// layout; w = sum x k is accumulated on the CUDA cores in the natural
+// layout (no x column in the tiles, so 32 features fit 4 blocks).
+template <int P, int NO, bool NAT = false>
 __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
@@ -639,7 +648,8 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
   const int R = a.rank;
   const int HS = R | 1;
   const int ld = a.ld;
-  float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R);
+  float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R, NAT);
+  float* kt = wbase + tc_ring_words(no, R) + W::batch_words(no);  // NAT: [8][kKtStride]
   uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
   float* st_x = wbase + no * W::kStage;                 // [kStage]
   uint32_t* rbat = reinterpret_cast<uint32_t*>(wbase + tc_ring_words(no, R));  // raw batches
@@ -655,19 +665,20 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
   constexpr bool QUAD = P == 4;   // ld == 32: one 128-byte row per pick and mode
   // feature of (lane group gg, block f) -- the rho -> feature map of K'
   auto feat = [&](int gg, int f) {
-    return QUAD ? 4 * gg + f : (f < 2 * NP ? 16 * (f / 2) + 2 * gg + (f & 1) : 16 * NP + gg);
+    return NAT ? gg + 8 * f : QUAD ? 4 * gg + f : (f < 2 * NP ? 16 * (f / 2) + 2 * gg + (f & 1) : 16 * NP + gg);
   };
   int xf = -1;  // block in which this lane holds the x column (feature R)
 #pragma unroll
   for (int f = 0; f < P; ++f)
-    if (feat(g, f) == R) xf = f;
+    if (!NAT && feat(g, f) == R) xf = f;
+  const int nq = lane >> 3, nsub = lane & 7;  // NAT: pick slot (and +4), feature quad
   const uint32_t ld4 = static_cast<uint32_t>(ld) * 4u;
 
   const float* ub2[NO];
   const float* ub1[NO];
 #pragma unroll
   for (int m = 0; m < NO; ++m) {
-    ub2[m] = a.U[m < no ? m : 0] + (QUAD ? 4 * g : 2 * g);
+    ub2[m] = a.U[m < no ? m : 0] + (NAT ? 4 * nsub : QUAD ? 4 * g : 2 * g);
     ub1[m] = a.U[m < no ? m : 0] + 16 * NP + g;
   }
 
@@ -727,9 +738,33 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
 
     int head = 0, cnt = 0;  // staging ring [head, head+cnt)
 
-    struct Raw {
+    struct RawPair {
       float f[NO][2][P];  // factor values (mode, pick, feature block)
       float x[2];
+    };
+    struct RawNat {
+      float4 v[2][NO];  // picks nq, nq + 4: features 4 nsub .. 4 nsub + 3 of each mode
+      float x[2];
+    };
+    using Raw = typename std::conditional<NAT, RawNat, RawPair>::type;
+    float4 wacc = make_float4(0.f, 0.f, 0.f, 0.f);  // NAT: w = sum x k, features 4 nsub..+3
+    auto load_nat = [&](int at, int np) {
+      RawNat r;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = nq + 4 * h;
+        const bool on = q < np;
+        const int sl = (at + q) & (W::kStage - 1);
+#pragma unroll
+        for (int m = 0; m < NO; ++m)
+          if (m < no) {
+            const uint32_t row = on ? st_o[m * W::kStage + sl] : 0u;
+            r.v[h][m] = __ldg(reinterpret_cast<const float4*>(row_ptr(ub2[m], row, ld4)));
+          }
+        r.x[h] = on ? st_x[sl] : 0.f;
+        if (!on) r.v[h][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      return r;
     };
     // gather of one group: np picks present (8 for full groups).  Quad layout
     // (P = 4, ld = 32): one 16-byte load per pick and mode, features 4g..4g+3
@@ -739,8 +774,8 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     // padding or the next row and land in discarded rows/cols of K'^T K'.
     // Group starts are multiples of 8 (head only advances by whole groups
     // inside an item), so the ring pair (q0, q0 + 1) is one 8-byte load.
-    auto load = [&](int at, int np) {
-      Raw r;
+    auto load_pair = [&](int at, int np) {
+      RawPair r;
       const int s0 = (at + q0) & (W::kStage - 1);
       const bool on0 = q0 < np, on1 = q0 + 1 < np;
 #pragma unroll
@@ -779,18 +814,63 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
         for (int f = 0; f < P; ++f) r.f[0][1][f] = 0.f;
       return r;
     };
+    auto load = [&](int at, int np) {
+      if constexpr (NAT)
+        return load_nat(at, np);
+      else
+        return load_pair(at, np);
+    };
+    // k values of this lane's two picks and feature blocks, fragment layout
+    auto kvals = [&](const Raw& r, float (&kf)[2][P]) {
+      if constexpr (NAT) {
+        // natural layout -> products -> shared tile -> fragment layout
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 k = r.v[h][0];
+#pragma unroll
+          for (int m = 1; m < NO; ++m)
+            if (m < no) {
+              k.x *= r.v[h][m].x;
+              k.y *= r.v[h][m].y;
+              k.z *= r.v[h][m].z;
+              k.w *= r.v[h][m].w;
+            }
+          wacc.x = fmaf(r.x[h], k.x, wacc.x);
+          wacc.y = fmaf(r.x[h], k.y, wacc.y);
+          wacc.z = fmaf(r.x[h], k.z, wacc.z);
+          wacc.w = fmaf(r.x[h], k.w, wacc.w);
+          *reinterpret_cast<float4*>(kt + (nq + 4 * h) * kKtStride + 4 * nsub) = k;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int f = 0; f < P; ++f) kf[q][f] = kt[(q0 + q) * kKtStride + g + 8 * f];
+        __syncwarp();  // the tile is rewritten by the next group
+      } else {
+#pragma unroll
+        for (int f = 0; f < P; ++f)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            float k = r.f[0][q][f];
+#pragma unroll
+            for (int m = 1; m < NO; ++m)
+              if (m < no) k *= r.f[m][q][f];
+            if (xf == f) k = r.x[q];  // the x column of k'
+            kf[q][f] = k;
+          }
+      }
+    };
     auto compute = [&](const Raw& r) {
       uint32_t hb[2][P], hp[P], lp[P];
+      float kf[2][P];
+      kvals(r, kf);
 #pragma unroll
       for (int f = 0; f < P; ++f) {
         float lo[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          float k = r.f[0][q][f];
-#pragma unroll
-          for (int m = 1; m < NO; ++m)
-            if (m < no) k *= r.f[m][q][f];
-          if (xf == f) k = r.x[q];  // the x column of k'
+          const float k = kf[q][f];
           hb[q][f] = __float_as_uint(k) & 0xffffe000u;
           lo[q] = k - __uint_as_float(hb[q][f]);
         }
@@ -920,12 +1000,29 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
         if (fr < R && fc < R) {
           Hf[fr * HS + fc] = v;
           Hf[fc * HS + fr] = v;
-        } else if (fr < R && fc == R) {
+        } else if (!NAT && fr < R && fc == R) {
           gd[fr] = static_cast<double>(v);
-        } else if (fc < R && fr == R) {
+        } else if (!NAT && fc < R && fr == R) {
           gd[fc] = static_cast<double>(v);
         }
       }
+    }
+    if constexpr (NAT) {
+      // w: sum the 4 pick slots holding the same features (lanes nsub + 8 q)
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1) {
+        wacc.x += __shfl_xor_sync(0xffffffffu, wacc.x, o);
+        wacc.y += __shfl_xor_sync(0xffffffffu, wacc.y, o);
+        wacc.z += __shfl_xor_sync(0xffffffffu, wacc.z, o);
+        wacc.w += __shfl_xor_sync(0xffffffffu, wacc.w, o);
+      }
+      if (nq == 0) {
+        const float wv[4] = {wacc.x, wacc.y, wacc.z, wacc.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * nsub + i < R) gd[4 * nsub + i] = static_cast<double>(wv[i]);
+      }
+      wacc = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncwarp();
     if (cur.slot < 0) {
@@ -1141,7 +1238,7 @@ static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, si
   return 1;
 }
 
-template <int P, int NO>
+template <int P, int NO, bool NAT = false>
 static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
   // Few items (a small tensor or a thin row shard): fewer warps per CTA so the
   // items spread over every SM instead of filling a few.
@@ -1155,15 +1252,15 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
   }();
   const int wpc = static_cast<int>(std::min<uint64_t>(wmax, std::max<uint64_t>(1, per_sm_items)));
   smem = warp_bytes * wpc;
-  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO>, wpc * 32, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT>, wpc * 32, smem));
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (pl.n_items + wpc - 1) / wpc;
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   grid = std::max<uint64_t>(grid, 1);
-  k_update_tc<P, NO><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
+  k_update_tc<P, NO, NAT><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
   return 1;
 }
@@ -1188,7 +1285,13 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // ranks 32-39 (P = 5) compile but stay on the CUDA-core kernel: at one CTA
   // per SM the pair-layout gathers of three factors measured 21 ms vs 17.6 ms
   // per mode on config 4
-  if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
+  static const bool nat_off = std::getenv("NTCB_NO_NAT") != nullptr;  // A/B switch
+  if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && a.rank >= 25 && (a.no == 2 || a.no == 3)) {
+    // ranks 25-32: natural-layout gathers through a shared tile into the
+    // tensor-core Gram (w on the CUDA cores)
+    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true)) * 4 * kWarps;
+    launches += a.no == 2 ? launch_items_tc<4, 2, true>(ctx, a, pl, ts) : launch_items_tc<4, 3, true>(ctx, a, pl, ts);
+  } else if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
     const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank)) * 4 * kWarps;
     launches += P == 1 ? launch_tc<1>(ctx, a, pl, ts)
               : P == 2 ? launch_tc<2>(ctx, a, pl, ts)
