@@ -39,6 +39,10 @@ CONFIGS = {
     3: dict(dims=[480189, 17770, 2182], nnz=100_000_000, true_rank=10, sigma=0.5, R=16, iters=10,
             zipf=[1.2, 1.2, 0.0], kind=1),
     4: dict(dims=[50000, 50000, 1000, 100], nnz=500_000_000, true_rank=32, sigma=0.01, R=32, iters=10),
+    # Zipf(1.1, 1.1, 1.3) over permuted ids, 1.7B cells: ~4.05e9 candidates
+    # (duplicates redrawn), ~61 GB of mode views -- fits one 180 GB B200
+    5: dict(dims=[4_800_000, 1_800_000, 1_800_000], nnz=1_700_000_000, true_rank=16, sigma=0.05, R=16,
+            iters=10, zipf=[1.1, 1.1, 1.3]),
 }
 
 
@@ -49,13 +53,36 @@ def generate(ctx, cfgd, cid):
 
 def workload_name(cid, c):
     d = "x".join(str(x) for x in c["dims"])
-    if c.get("kind", 0) == 1:
+    if c.get("zipf") and c.get("kind", 0) == 0:
+        vals = (f"modes Zipf{tuple(c['zipf'])} over permuted ids, truth rank {c['true_rank']} U[0,1) "
+                f"+ N(0,{c['sigma']}^2) clamped>=0")
+    elif c.get("kind", 0) == 1:
         vals = (f"modes Zipf{tuple(c['zipf'])} over permuted ids, ratings round(clip(1+4*CPD_r{c['true_rank']}/"
                 f"{c['true_rank']} + N(0,{c['sigma']}^2), 1, 5))")
     else:
         vals = f"uniform cells, truth rank {c['true_rank']} U[0,1) + N(0,{c['sigma']}^2) clamped>=0"
     return f"cfg{cid}: {d}, nnz={c['nnz']}, {vals}, fit rank {c['R']}, c=0.5, MAX_INNER=1, lambda=1e-3"
 
+
+
+def l2_note(c, l2_bytes=126 * 2**20):
+    """Per-mode view bytes against the L2 size (the timing rule asks which holds)."""
+    N = len(c["dims"])
+    view = 4 * N * c["nnz"]
+    if view > l2_bytes:
+        return (f"inputs larger than L2: each mode update streams its {view / 1e9:.2f} GB view "
+                f"({4 * N} B/entry x {c['nnz']}), no flush needed")
+    return (f"inputs fit in L2 ({view / 1e6:.0f} MB per mode view), not flushed: a latency/parity case, "
+            f"not the headline")
+
+
+def update_kernel_name(R, order):
+    """The update kernel update.cu:launch_ld dispatches to."""
+    if 25 <= R <= 32 and order in (3, 4):
+        return "k_update_tc NAT (natural-layout gathers + tensor-core Hessian + power method + step)"
+    if R <= 31 and order <= 4:
+        return "k_update_tc (gradient + tensor-core Hessian + power method + step)"
+    return "k_update (gradient + CUDA-core Hessian + power method + step)"
 
 
 def peaks():
@@ -277,6 +304,14 @@ def run_ours(args, cfgd, cid):
     hbm, peak_src = peaks()
     N = order
     alg_bytes = 4 * N * full + (16 * R + 8) * rows_processed  # per sweep, SURVEY.md §8(d)
+    # + (N-1) 4R B of factor-row gathers per sampled nnz in the modes whose
+    # other factors exceed L2 (config 5 only)
+    gather_modes = []
+    for m in range(order):
+        other = sum(dims[q] * R * 4 for q in range(order) if q != m)
+        if other > 126 * 2**20:
+            alg_bytes += (N - 1) * 4 * R * int(blocksizes(offs[m], cfg.c).sum())
+            gather_modes.append(m)
     per_launch_bytes = alg_bytes / order
     avg_upd_s = (upd_ms / max(upd_launches, 1)) / 1000.0
     achieved = per_launch_bytes / avg_upd_s / 1e9
@@ -291,7 +326,7 @@ def run_ours(args, cfgd, cid):
                "achieved_tflops": flops_launch / avg_upd_s / 1e12,
                "fp32_peak_tflops": fp32_peak, "fp32_peak_source": "measured FFMA, tools/microbench/hmma.cu",
                "frac_fp32": flops_launch / avg_upd_s / 1e12 / fp32_peak}
-    limiter = {"unit": "L1/LSU data pipe (two factor-row gathers from L2 per sampled nnz; Gram on tensor cores)",
+    limiter = {"unit": f"L1/LSU data pipe ({N - 1} factor-row gathers per sampled nnz; Gram on tensor cores)",
                "util": None, "dram_util": None, "source": None}
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json")
@@ -385,15 +420,14 @@ def run_ours(args, cfgd, cid):
                        "exchange": (sharded.exchange if sharded else "none"),
                        "rank": R, "c": 0.5, "max_inner": 1, "lambda": 1e-3,
                        "sampled_per_ao_iteration": full,
-                       "l2": "inputs larger than L2: views stream 12 B/entry x 100M per mode per iteration",
+                       "l2": l2_note(cfgd),
                        "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
             "sec_per_ao_iteration": ms / args.steps / 1000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": ("k_update_tc (gradient + tensor-core Hessian + power method + step)"
-                                    if R <= 31 and order <= 4 else
-                                    "k_update (gradient + CUDA-core Hessian + power method + step)"),
+                         "kernel": update_kernel_name(R, order),
                          "alg_bytes_per_launch": per_launch_bytes,
+                         "gathers_counted_in_modes": gather_modes,
                          "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)
                          # side-stream spans include queueing behind the update: not busy time
                          "sampler_span_ms_per_step": smp_ms / args.steps,

@@ -39,8 +39,10 @@ struct Buf {
   explicit Buf(size_t n) {
     if (n) NTCB_CUDA(cudaMalloc(&p, sizeof(T) * n));
   }
-  ~Buf() {
+  ~Buf() { release(); }
+  void release() {
     if (p) cudaFree(p);
+    p = nullptr;
   }
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
@@ -246,10 +248,15 @@ void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
     d.perm[m] = d_perm[m];
   }
 
+  // Candidate ids are u32 (sort payload): at most 2^32 - 2 candidates per
+  // device.  Config 5 (1.7B cells of a Zipf(1.1, 1.1, 1.3) product) needs
+  // ~4.05e9 of them -- the retry policy below clamps to the cap instead of
+  // overshooting it, so that tensor still fits one device.
+  constexpr uint64_t kMaxCand = (1ull << 32) - 2;
   uint64_t M = nnz + std::max<uint64_t>(nnz / 256, 4096);
   Buf<uint32_t> chosen(nnz);
   for (int attempt = 0;; ++attempt) {
-    if (M >= (1ull << 32) - 1) fail(NTCB_EINVAL, "synth: too many candidates (duplicate-heavy distribution)");
+    if (M > kMaxCand) fail(NTCB_EINVAL, "synth: too many candidates (duplicate-heavy distribution)");
     Buf<uint64_t> key(M), key2(M);
     Buf<uint32_t> jj(M), jj2(M);
     k_candidates<<<grid_of(M, sms), 256, 0, st>>>(s_mask, M, d, key.p, jj.p);
@@ -271,7 +278,10 @@ void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
     if (uniq < nnz) {
       const double frac = static_cast<double>(uniq) / static_cast<double>(M);
       uint64_t next = static_cast<uint64_t>(static_cast<double>(nnz) / std::max(frac, 1e-3) * 1.05) + 4096;
-      M = std::max<uint64_t>(next, M + M / 4);
+      next = std::max<uint64_t>(next, M + M / 4);
+      // the unique fraction falls as M grows: one last try at the cap
+      if (next > kMaxCand && M < kMaxCand) next = kMaxCand;
+      M = next;
       continue;
     }
     // ascending j; skipped entries carry 0xffffffff and sort last
@@ -287,6 +297,13 @@ void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
 
   const int R = static_cast<int>(true_rank);
   std::vector<double*> truth(order, nullptr);
+  struct TruthCleanup {
+    std::vector<double*>& t;
+    ~TruthCleanup() {
+      for (double* p : t)
+        if (p) cudaFree(p);
+    }
+  } truth_cleanup{truth};
   for (int m = 0; m < order; ++m) {
     NTCB_CUDA(cudaMalloc(&truth[m], sizeof(double) * dims[m] * R));
     k_truth<<<grid_of(dims[m] * R, sms), 256, 0, st>>>(fork64(fork64(seed, 4), m), dims[m] * R,
@@ -301,7 +318,11 @@ void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t 
                                             sigma, kind, idx.p, vals.p);
   NTCB_CUDA(cudaGetLastError());
   NTCB_CUDA(cudaStreamSynchronize(st));
-  for (double* p : truth) cudaFree(p);
+  for (double*& p : truth) {
+    cudaFree(p);
+    p = nullptr;
+  }
+  chosen.release();  // the tensor build of a 1.7B-entry tensor needs the room
   load_tensor_f32(ctx, order, dims, nnz, idx.p, vals.p, true);
 }
 

@@ -275,7 +275,10 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
   for (int m = 0; m < order; ++m) ctx->dims[m] = dims[m];
 
   // ---- per-mode stable views -------------------------------------------------
-  DevBuf<uint32_t> mperm(nnz), mperm_alt(nnz);
+  // (the lexicographic pass's alternate buffer is free now: it is the mode
+  // sorts' alternate, so a 1.7B-entry tensor builds within one device)
+  DevBuf<uint32_t> mperm(nnz);
+  uint32_t* mperm_alt = perm_alt.p;
   uint32_t* mkey = reinterpret_cast<uint32_t*>(key.p);      // reuse as u32 buffers
   uint32_t* mkey_alt = reinterpret_cast<uint32_t*>(key_alt.p);
   DevBuf<uint32_t*> d_oth(NTCB_MAX_ORDER);
@@ -289,7 +292,7 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
       NTCB_CUDA(cudaMemcpyAsync(mperm.p, perm.p, sizeof(uint32_t) * nnz, cudaMemcpyDeviceToDevice, st));
       k_mode_keys<<<grid_for(nnz, sms), 256, 0, st>>>(d_idx, mperm.p, nnz, order, m, mkey);
       NTCB_CUDA(cudaGetLastError());
-      if (m != 0) radix_pairs<uint32_t>(ctx, mkey, mkey_alt, mperm.p, mperm_alt.p, nnz, bits_for(dims[m]));
+      if (m != 0) radix_pairs<uint32_t>(ctx, mkey, mkey_alt, mperm.p, mperm_alt, nnz, bits_for(dims[m]));
       k_offsets<<<grid_for(v.rows + 1, sms), 256, 0, st>>>(mkey, nnz, v.rows, v.off);
       NTCB_CUDA(cudaGetLastError());
       NTCB_CUDA(cudaMemcpyAsync(d_oth.p, v.oth, sizeof(uint32_t*) * NTCB_MAX_ORDER,
