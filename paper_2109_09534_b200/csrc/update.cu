@@ -698,8 +698,10 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
         }
       }
-      if (!full) {
-        const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + lane));
+      // one mask word per 32 entries: lanes 8i copy word i (the other lanes
+      // of the octet would copy the same word -- 8-way shared conflicts)
+      if (!full && (lane & 7) == 0) {
+        const unsigned dm = static_cast<unsigned>(__cvta_generic_to_shared(rmsk + buf * 32 + (lane >> 3)));
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dm), "l"(a.mask + (e >> 5)));
       }
     }
@@ -947,7 +949,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
         if (m < no) co[m] = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + m) * 128)[lane];
       const uint4 cv = reinterpret_cast<const uint4*>(rbat + (buf * (no + 1) + no) * 128)[lane];
       const int r = t0 + 4 * lane;
-      uint32_t bits = full ? 0xfu : (rmsk[buf * 32 + lane] >> ((sh0 + static_cast<uint32_t>(r)) & 31u)) & 0xfu;
+      uint32_t bits = full ? 0xfu : (rmsk[buf * 32 + (lane >> 3)] >> ((sh0 + static_cast<uint32_t>(r)) & 31u)) & 0xfu;
       if (r < lo) bits &= 0xfu << (lo - r);
       if (r + 4 > hi) bits &= hi - r > 0 ? (0xfu >> (4 - (hi - r))) : 0u;
       const int c4 = __popc(bits);
@@ -1281,7 +1283,11 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   int launches = 0;
   // feature blocks of k' = (k, x), pair layout (the 16-byte quad layout reads
   // whole 128-byte rows and measured 40% slower at rank 20)
-  const int P = (a.rank + 1 + 7) / 8;
+  int P = (a.rank + 1 + 7) / 8;
+  // experiment knob: NTCB_TC_P=4 runs the quad layout (one 16-byte load per
+  // pick and mode, features 4g..4g+3) at any rank <= 31
+  static const int p_env = [] { const char* e = std::getenv("NTCB_TC_P"); return e ? std::atoi(e) : 0; }();
+  if (p_env > P && p_env <= 4) P = p_env;
   // ranks 32-39 (P = 5) compile but stay on the CUDA-core kernel: at one CTA
   // per SM the pair-layout gathers of three factors measured 21 ms vs 17.6 ms
   // per mode on config 4

@@ -611,3 +611,67 @@ def test_cfg2_scale_properties(ntc, orc):
     ctx.collect()
     for m in range(3):
         np.testing.assert_array_equal(ctx.get_factor(m)[0], A1[m])
+
+
+# BASELINE configs[2..4] at full size, generated as bench.py does (seed 1000 + id)
+_FULL = {
+    3: dict(dims=[480189, 17770, 2182], nnz=100_000_000, true_rank=10, sigma=0.5, R=16,
+            zipf=[1.2, 1.2, 0.0], kind=1),
+    4: dict(dims=[50000, 50000, 1000, 100], nnz=500_000_000, true_rank=32, sigma=0.01, R=32),
+    5: dict(dims=[4_800_000, 1_800_000, 1_800_000], nnz=1_700_000_000, true_rank=16, sigma=0.05, R=16,
+            zipf=[1.1, 1.1, 1.3]),
+}
+
+
+@pytest.mark.parametrize("cid", [3, 4, 5])
+def test_full_scale_properties(ntc, orc, cid):
+    """Configs 3-5 at their BASELINE sizes (config 5: 1.7B entries, a
+    437M-entry slice in mode 2) through size-independent invariants, on the
+    mode holding the longest slice: per-row popcounts of the sampled set equal
+    floor(c n) for every row; the five longest rows (heavy grid sampler) and
+    twelve random rows (warp / CTA samplers) bit-exact against the reference's
+    Fisher-Yates picks; a sweep accesses sum(b_p), keeps factors nonnegative,
+    lowers the relative error and is deterministic to the bit."""
+    import gc
+    import paper_2109_09534_b200 as P
+    c = _FULL[cid]
+    dims, R = c["dims"], c["R"]
+    N = len(dims)
+    ctx = P.Context(0)
+    try:
+        ctx.synth(dims, c["nnz"], c["true_rank"], c["sigma"], 1000 + cid, c.get("zipf"), c.get("kind", 0))
+        assert ctx.info()[2] == c["nnz"]
+        offs = [ctx.view_offsets(m).astype(np.int64) for m in range(N)]
+        mode = int(np.argmax([np.diff(o).max() for o in offs]))
+        off = offs[mode]
+        n = np.diff(off)
+        b = np.floor(0.5 * n.astype(np.float64)).astype(np.int64)
+        st = 0xC0FFEE + cid
+        e0, bits = ctx.sample_mask(mode, 0.5, st, 0)
+        assert e0 == 0
+        cnt = np.add.reduceat(bits, np.minimum(off[:-1], c["nnz"] - 1), dtype=np.int64)
+        cnt[n == 0] = 0
+        np.testing.assert_array_equal(cnt, b)
+        rng = np.random.default_rng(cid)
+        rows = np.argsort(n)[-5:].tolist() + rng.choice(np.flatnonzero(n > 0), 12, replace=False).tolist()
+        for p in rows:
+            want = np.zeros(int(n[p]), bool)
+            want[orc.sample_row(int(n[p]), 0.5, orc.fork(orc.fork(st, 0), p))] = True
+            np.testing.assert_array_equal(bits[off[p]:off[p + 1]], want, err_msg=f"row {p} (n={n[p]})")
+        del bits, want
+        expect = sum(int(np.floor(0.5 * np.diff(o.astype(np.float64))).sum()) for o in offs)
+        ctx.random_factors(R, 7)
+        r0 = ctx.relative_error()
+        ctx.sweep_async(0, P.NmcConfig(c=0.5), 7)
+        assert ctx.collect() == expect
+        A1 = [ctx.get_factor(m)[0] for m in range(N)]
+        assert ctx.relative_error() < r0
+        assert all(np.all(a >= 0) for a in A1)
+        ctx.random_factors(R, 7)
+        ctx.sweep_async(0, P.NmcConfig(c=0.5), 7)
+        ctx.collect()
+        for m in range(N):
+            np.testing.assert_array_equal(ctx.get_factor(m)[0], A1[m])
+    finally:
+        ctx.close()
+        gc.collect()
