@@ -706,6 +706,12 @@ __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags
   }
 }
 
+// Chain walks are dependent reads: each warp takes kTailIlp mask words at
+// once and walks their chains in lockstep (kTailIlp independent reads in
+// flight per lane).  Chains are disjoint (the last draw targeting a position
+// is unique to it), so each root has one writer.
+constexpr int kTailIlp = 4;
+
 __global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int* flags,
                              uint32_t* mask) {
   const HeavyRow h = rows[blockIdx.y];
@@ -715,21 +721,46 @@ __global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int*
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = gb0 >> 5, w1 = (gb1 - 1) >> 5;
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
-    const uint64_t g = (w << 5) + lane;
-    const bool valid = g >= gb0 && g < gb1;
-    const uint32_t tv = valid ? (scratch[g] & 0x7fffffffu) : 0u;
-    if (tv) {
-      uint32_t v = tv - 1, nx;
-      while ((nx = scratch[h.beg + v] & 0x7fffffffu) != 0u) v = nx - 1;
-      scratch[h.beg + v] = 0x80000000u;  // unpicked root
+  const uint32_t* sc = scratch + h.beg;
+  for (uint64_t wb = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); wb <= w1;
+       wb += kTailIlp * nwarps) {
+    uint32_t v[kTailIlp];
+    bool walk[kTailIlp];
+#pragma unroll
+    for (int i = 0; i < kTailIlp; ++i) {
+      const uint64_t w = wb + i * nwarps;
+      const uint64_t g = (w << 5) + lane;
+      const bool valid = w <= w1 && g >= gb0 && g < gb1;
+      const uint32_t tv = valid ? (scratch[g] & 0x7fffffffu) : 0u;
+      walk[i] = tv != 0u;
+      v[i] = tv - 1;
+      const uint32_t bits = __ballot_sync(kFull, walk[i]);
+      if (lane == 0 && w <= w1) {
+        if ((w << 5) >= gb0 && (w << 5) + 32 <= gb1)
+          mask[w] = bits;
+        else if (bits)
+          atomicOr(&mask[w], bits);
+      }
     }
-    const uint32_t bits = __ballot_sync(kFull, tv != 0u);
-    if (lane == 0) {
-      if ((w << 5) >= gb0 && (w << 5) + 32 <= gb1)
-        mask[w] = bits;
-      else if (bits)
-        atomicOr(&mask[w], bits);
+    // chains: v -> T[v] - 1 until T[v] == 0 (the unpicked root)
+    bool any = true;
+    while (any) {
+      uint32_t nx[kTailIlp];
+#pragma unroll
+      for (int i = 0; i < kTailIlp; ++i) nx[i] = walk[i] ? (sc[v[i]] & 0x7fffffffu) : 0u;
+      any = false;
+#pragma unroll
+      for (int i = 0; i < kTailIlp; ++i) {
+        if (walk[i]) {
+          if (nx[i] != 0u) {
+            v[i] = nx[i] - 1;
+            any = true;
+          } else {
+            scratch[h.beg + v[i]] = 0x80000000u;  // unpicked root
+            walk[i] = false;
+          }
+        }
+      }
     }
   }
 }
@@ -770,8 +801,12 @@ __global__ void k_heavy_exact(const HeavyRow* rows, uint32_t* scratch, const int
                             nullptr, mask, h.beg, nullptr);
 }
 
-static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>,
-                std::pair<HeavyRow*, uint32_t>> g_heavy;
+struct HeavyPlan {
+  HeavyRow* first;
+  uint32_t second;  // slices
+  uint64_t third;   // longest slice
+};
+static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>, HeavyPlan> g_heavy;
 
 int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
                         uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
@@ -798,8 +833,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       NTCB_CUDA(cudaMalloc(&d, sizeof(HeavyRow) * (hr.size() + 1)));
       NTCB_CUDA(cudaMemcpy(d, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
     }
-    it = g_heavy.emplace(key, std::make_pair(d, static_cast<uint32_t>(hr.size()))).first;
-    (void)maxn;
+    it = g_heavy.emplace(key, HeavyPlan{d, static_cast<uint32_t>(hr.size()), maxn}).first;
   }
   const uint32_t nh = it->second.second;
   if (nh == 0) return 0;
@@ -811,11 +845,22 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     ctx->heavy_flags_n = nh;
   }
   const HeavyRow* d = it->second.first;
-  const dim3 grid(static_cast<unsigned>(ctx->sm_count * 2), nh);
-  k_heavy_zero<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
-  k_heavy_draw<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
-  k_heavy_tail<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
-  k_heavy_head<<<grid, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  // (chunk, slice) grids: 2 x SMs CTAs per slice at most, fewer when the
+  // longest slice gives each thread less than ~kPer entries -- slices of a
+  // few hundred thousand entries otherwise launch ~300 mostly idle CTAs
+  // each (config 4: 1000 slices of 500K entries, CTA-launch bound; kPer = 8 measured
+  // best: config 4 tail phase 5.06 -> 2.40 ms per mode).
+  // NTCB_HEAVY_PER overrides kPer for experiments.
+  static const uint64_t per = [] { const char* e = std::getenv("NTCB_HEAVY_PER"); return e ? std::max(1, std::atoi(e)) : 8; }();
+  const uint64_t maxn = it->second.third;
+  auto gx = [&](uint64_t work) {
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
+  };
+  const dim3 gz(gx(maxn), nh), gd(gx((maxn + 1) / 2), nh), gt(gx((maxn + 1) / 2 / kTailIlp), nh), gh(gx((maxn + 1) / 2), nh);
+  k_heavy_zero<<<gz, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
+  k_heavy_draw<<<gd, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
+  k_heavy_tail<<<gt, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  k_heavy_head<<<gh, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
   k_heavy_exact<<<nh, 32, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask, root, direct);
   NTCB_CUDA(cudaGetLastError());
   return 5;
