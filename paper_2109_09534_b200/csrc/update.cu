@@ -52,7 +52,19 @@ struct FinItem {
   uint64_t row;
   int64_t slot0;
   int32_t nslots;
+  int32_t ngroups;  // big rows: slot groups of kSlotGroup, sums at gpart[g0 ..]
+  int64_t g0;
 };
+
+// a group of <= kSlotGroup consecutive slots of a big split row, summed in
+// slot order (fp64) by one warp of k_slot_groups into gpart[out]
+struct SlotGroup {
+  int64_t slot0;
+  int64_t out;
+  int32_t n;
+  int32_t pad;
+};
+constexpr int kSlotGroup = 32;
 
 struct UpdateArgs {
   const uint64_t* off;
@@ -73,6 +85,9 @@ struct UpdateArgs {
   const FinItem* fins;
   uint64_t n_fins;
   float* partial;  // [slot][R*R + R]
+  double* gpart;   // [group][R*R + R]: slot-group sums of big split rows
+  const SlotGroup* groups;
+  uint64_t n_groups;
   double c;
   double lambda;
   double power_tol;
@@ -1096,6 +1111,44 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize_small(UpdateArgs a) {
 }
 
 
+// Big split rows, level 1: a warp per group of <= kSlotGroup consecutive
+// slots sums them in slot order (fp64), 4 elements per lane and 4 slots in
+// flight; the whole grid works on the groups of every big row at once (one
+// CTA per row summing thousands of slots serially took 1.5 ms for a 9M-entry
+// row of config 3 and 5.5 ms per mode-2 update of config 5).
+__global__ void __launch_bounds__(kWarps * 32) k_slot_groups(UpdateArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int NE = a.rank * a.rank + a.rank;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kWarps;
+  for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(kWarps) + (threadIdx.x >> 5); gi < a.n_groups; gi += nw) {
+    const SlotGroup gr = a.groups[gi];
+    const float* base = a.partial + static_cast<uint64_t>(gr.slot0) * NE;
+    double* out = a.gpart + static_cast<uint64_t>(gr.out) * NE;
+    for (int i0 = 0; i0 < NE; i0 += 128) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int q = 0; q < gr.n; q += 4) {
+        float v[4][4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u + lane;
+            v[qq][u] = (q + qq < gr.n && i < NE) ? base[static_cast<uint64_t>(q + qq) * NE + i] : 0.f;
+          }
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(v[qq][u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + 32 * u + lane;
+        if (i < NE) out[i] = acc[u];
+      }
+    }
+  }
+}
+
 template <int LD4>
 __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
   using W = WarpSmem<LD4>;
@@ -1112,19 +1165,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
   for (uint64_t f = blockIdx.x; f < a.n_fins; f += gridDim.x) {
     if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
     const FinItem fi = a.fins[f];
-    const int chunk = (fi.nslots + kWarps - 1) / kWarps;
-    const int qa = wid * chunk, qb = min(fi.nslots, qa + chunk);
+    // the row's slot-group sums (k_slot_groups), contiguous group ranges per
+    // warp, combined in warp order below
+    const int chunk = (fi.ngroups + kWarps - 1) / kWarps;
+    const int qa = wid * chunk, qb = min(fi.ngroups, qa + chunk);
     for (int e0 = 0; e0 < NE; e0 += kFinPass) {
       double acc[kFinPass / 32];
 #pragma unroll
       for (int u = 0; u < kFinPass / 32; ++u) acc[u] = 0.0;
       for (int q = qa; q < qb; ++q) {
-        const float* src = a.partial + static_cast<uint64_t>(fi.slot0 + q) * NE + e0;
-        float v[kFinPass / 32];
+        const double* src = a.gpart + static_cast<uint64_t>(fi.g0 + q) * NE + e0;
+        double v[kFinPass / 32];
 #pragma unroll
-        for (int u = 0; u < kFinPass / 32; ++u) v[u] = (e0 + 32 * u + lane < NE) ? src[32 * u + lane] : 0.f;
+        for (int u = 0; u < kFinPass / 32; ++u) v[u] = (e0 + 32 * u + lane < NE) ? src[32 * u + lane] : 0.0;
 #pragma unroll
-        for (int u = 0; u < kFinPass / 32; ++u) acc[u] += static_cast<double>(v[u]);
+        for (int u = 0; u < kFinPass / 32; ++u) acc[u] += v[u];
       }
 #pragma unroll
       for (int u = 0; u < kFinPass / 32; ++u) P[wid * kFinPass + 32 * u + lane] = acc[u];
@@ -1152,7 +1207,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
 struct WorkPlan {
   WorkItem* d_items = nullptr;
   FinItem* d_fins = nullptr;  // [n_small small rows][n_fins - n_small big rows]
-  uint64_t n_items = 0, n_fins = 0, n_slots = 0, n_small = 0;
+  SlotGroup* d_groups = nullptr;
+  uint64_t n_items = 0, n_fins = 0, n_slots = 0, n_small = 0, n_groups = 0;
 };
 static std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan> g_plans;
 
@@ -1181,7 +1237,7 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
       items.push_back({p, off[p], off[p + 1], -1});
     } else {
       const uint64_t ns = (n + seg - 1) / seg;
-      fins.push_back({p, slot, static_cast<int32_t>(ns)});
+      fins.push_back({p, slot, static_cast<int32_t>(ns), 0, 0});
       for (uint64_t s = 0; s < ns; ++s)
         items.push_back({p, off[p] + s * seg, std::min(off[p + 1], off[p] + (s + 1) * seg), slot++});
     }
@@ -1197,6 +1253,20 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   pl.n_small = static_cast<uint64_t>(
       std::count_if(fins.begin(), fins.end(), [](const FinItem& f) { return f.nslots <= kFinSmall; }));
   pl.n_slots = static_cast<uint64_t>(slot);
+  std::vector<SlotGroup> groups;
+  for (auto& f : fins) {
+    if (f.nslots <= kFinSmall) continue;
+    f.g0 = static_cast<int64_t>(groups.size());
+    f.ngroups = (f.nslots + kSlotGroup - 1) / kSlotGroup;
+    for (int32_t g = 0; g < f.ngroups; ++g)
+      groups.push_back({f.slot0 + static_cast<int64_t>(g) * kSlotGroup, f.g0 + g,
+                        std::min<int32_t>(kSlotGroup, f.nslots - g * kSlotGroup), 0});
+  }
+  pl.n_groups = groups.size();
+  if (pl.n_groups) {
+    NTCB_CUDA(cudaMalloc(&pl.d_groups, sizeof(SlotGroup) * pl.n_groups));
+    NTCB_CUDA(cudaMemcpy(pl.d_groups, groups.data(), sizeof(SlotGroup) * pl.n_groups, cudaMemcpyHostToDevice));
+  }
   if (pl.n_items) {
     NTCB_CUDA(cudaMalloc(&pl.d_items, sizeof(WorkItem) * pl.n_items));
     NTCB_CUDA(cudaMemcpy(pl.d_items, items.data(), sizeof(WorkItem) * pl.n_items, cudaMemcpyHostToDevice));
@@ -1216,6 +1286,7 @@ void drop_plans(ntcb_context* ctx) {
     if (mine) {
       if (it->second.d_items) cudaFree(it->second.d_items);
       if (it->second.d_fins) cudaFree(it->second.d_fins);
+      if (it->second.d_groups) cudaFree(it->second.d_groups);
       it = g_plans.erase(it);
     } else {
       ++it;
@@ -1323,6 +1394,12 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
     NTCB_CUDA(cudaGetLastError());
     ++launches;
   }
+  if (pl.n_groups) {  // big rows, level 1: slot groups over the whole grid
+    const uint64_t gg = std::min<uint64_t>((pl.n_groups + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_slot_groups<<<static_cast<unsigned>(gg), kWarps * 32, 0, ctx->stream>>>(a);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
   if (pl.n_fins > pl.n_small) {  // CTA per row
     // warp 0's row-end layout + the per-warp partial sums of one pass
     const size_t fsmem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
@@ -1347,7 +1424,9 @@ int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_
   if (pl.n_items == 0) return 0;
   const uint64_t R = ctx->rank;
   if (pl.n_slots) {
-    const uint64_t need = pl.n_slots * (R * R + R);
+    // slots (fp32), then the slot-group sums (fp64) of the big rows
+    const uint64_t slot_words = (pl.n_slots * (R * R + R) + 1) & ~1ull;
+    const uint64_t need = slot_words + 2 * pl.n_groups * (R * R + R);
     if (ctx->partial_n < need) {
       if (ctx->partial) cudaFree(ctx->partial);
       NTCB_CUDA(cudaMalloc(&ctx->partial, sizeof(float) * need));
@@ -1378,6 +1457,9 @@ int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_
   a.fins = pl.d_fins;
   a.n_fins = pl.n_fins;
   a.partial = ctx->partial;
+  a.gpart = pl.n_groups ? reinterpret_cast<double*>(ctx->partial + ((pl.n_slots * (R * R + R) + 1) & ~1ull)) : nullptr;
+  a.groups = pl.d_groups;
+  a.n_groups = pl.n_groups;
   a.c = cfg.c;
   a.lambda = cfg.lambda;
   a.power_tol = cfg.power_tol;
