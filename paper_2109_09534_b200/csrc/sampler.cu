@@ -712,6 +712,88 @@ __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags
 // is unique to it), so each root has one writer.
 constexpr int kTailIlp = 4;
 
+// Slices whose scratch exceeds L2 (config 5: up to 261M entries): the draw
+// phase in target windows [w0, w1) of kWin entries, one slice and one window
+// per launch, so the atomics stay in L2.  Every draw j < min(b, w1) is
+// recomputed per window (only those can land there, r_j >= j) -- cheap
+// integer work instead of random DRAM read-modify-writes.
+__global__ void k_heavy_draw_win(const HeavyRow* rows, uint32_t* scratch, int* flags, uint64_t root,
+                                 int direct, uint32_t w0, uint32_t w1, uint32_t* tb) {
+  const HeavyRow h = rows[0];
+  const uint64_t state = direct ? root : fork64(root, h.row);
+  const uint32_t jend = min(h.b, w1);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jend; j += gridDim.x * blockDim.x) {
+    const uint32_t bound = h.n - j;
+    const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
+    const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
+    const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
+    if (static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound) flags[0] = 1;
+    const uint32_t r = j + static_cast<uint32_t>(u >> 32);
+    if (r >= w0 && r < w1 && r != j) {
+      atomicMax(&scratch[h.beg + r], j + 1);
+      if (r < h.b) atomicOr(&tb[r >> 5], 1u << (r & 31u));  // head position targeted: T[r] != 0
+    }
+  }
+}
+
+// Tail and head phases of one slice longer than the draw window.  Chain
+// steps consult the L2-resident bitmap `tb` (bit v: T[v] != 0, v < b) before
+// touching the DRAM-resident table, so the ~3/4 of chains that end at their
+// first node cost no random DRAM read; roots go to the bitmap `rb` (atomicOr
+// in L2) instead of bit 31 of the table, and the head phase reads `rb`.
+__global__ void k_heavy_tail_big(const HeavyRow* rows, const uint32_t* scratch, const int* flags, uint32_t* mask,
+                                 const uint32_t* tb, uint32_t* rb) {
+  const HeavyRow h = rows[0];
+  if (flags[0]) return;
+  const uint64_t gb0 = h.beg + h.b, gb1 = h.beg + h.n;
+  if (gb1 <= gb0) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = gb0 >> 5, w1 = (gb1 - 1) >> 5;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t* sc = scratch + h.beg;
+  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
+    const uint64_t g = (w << 5) + lane;
+    const bool valid = g >= gb0 && g < gb1;
+    const uint32_t tv = valid ? (scratch[g] & 0x7fffffffu) : 0u;
+    if (tv) {
+      uint32_t v = tv - 1;
+      while ((tb[v >> 5] >> (v & 31u)) & 1u) v = (sc[v] & 0x7fffffffu) - 1;
+      atomicOr(&rb[v >> 5], 1u << (v & 31u));  // unpicked root (chains are disjoint)
+    }
+    const uint32_t bits = __ballot_sync(kFull, tv != 0u);
+    if (lane == 0) {
+      if ((w << 5) >= gb0 && (w << 5) + 32 <= gb1)
+        mask[w] = bits;
+      else if (bits)
+        atomicOr(&mask[w], bits);
+    }
+  }
+}
+
+__global__ void k_heavy_head_big(const HeavyRow* rows, const int* flags, uint32_t* mask, const uint32_t* rb) {
+  const HeavyRow h = rows[0];
+  if (flags[0] || h.b == 0) return;
+  const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
+    const uint64_t g = (w << 5) + lane;
+    bool pick = false;
+    if (g >= ga0 && g < ga1) {
+      const uint64_t v = g - h.beg;
+      pick = !((rb[v >> 5] >> (v & 31u)) & 1u);
+    }
+    const uint32_t bits = __ballot_sync(kFull, pick);
+    if (lane == 0) {
+      if ((w << 5) >= ga0 && (w << 5) + 32 <= ga1)
+        mask[w] = bits;
+      else if (bits)
+        atomicOr(&mask[w], bits);
+    }
+  }
+}
+
 __global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int* flags,
                              uint32_t* mask) {
   const HeavyRow h = rows[blockIdx.y];
@@ -805,7 +887,26 @@ struct HeavyPlan {
   HeavyRow* first;
   uint32_t second;  // slices
   uint64_t third;   // longest slice
+  uint32_t n_reg;   // slices [0, n_reg) draw in one pass; the rest (host copies in `giant`) by windows
+  std::vector<HeavyRow> giant;
+  uint32_t* bits = nullptr;       // per giant slice: tb and rb bitmaps over [0, b)
+  std::vector<uint64_t> bit_off;  // word offset of giant slice i's tb (rb follows)
+  uint64_t bit_words = 0;
 };
+static uint32_t heavy_big() {  // NTCB_HEAVY_BIG: log2 of the slice length above which the bitmap path runs
+  static const uint32_t w = [] {
+    const char* e = std::getenv("NTCB_HEAVY_BIG");
+    return 1u << (e ? std::max(16, std::min(30, std::atoi(e))) : 24);
+  }();
+  return w;
+}
+static uint32_t heavy_window() {  // NTCB_HEAVY_WIN: log2 of the draw window (entries)
+  static const uint32_t w = [] {
+    const char* e = std::getenv("NTCB_HEAVY_WIN");
+    return 1u << (e ? std::max(16, std::min(30, std::atoi(e))) : 24);
+  }();
+  return w;
+}
 static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>, HeavyPlan> g_heavy;
 
 int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
@@ -828,12 +929,27 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
         maxn = std::max<uint32_t>(maxn, static_cast<uint32_t>(n));
       }
     }
-    HeavyRow* d = nullptr;
-    if (!hr.empty()) {
-      NTCB_CUDA(cudaMalloc(&d, sizeof(HeavyRow) * (hr.size() + 1)));
-      NTCB_CUDA(cudaMemcpy(d, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
+    // slices whose table is too long to stay in L2 alongside its neighbours
+    // go last: windowed draws, bitmap-assisted tail and head, one per launch
+    const uint32_t big = std::min(heavy_big(), heavy_window());
+    std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
+    HeavyPlan pl{nullptr, static_cast<uint32_t>(hr.size()), maxn, 0, {}};
+    for (const HeavyRow& h : hr) {
+      if (h.n <= big)
+        ++pl.n_reg;
+      else
+        pl.giant.push_back(h);
     }
-    it = g_heavy.emplace(key, HeavyPlan{d, static_cast<uint32_t>(hr.size()), maxn}).first;
+    for (const HeavyRow& h : pl.giant) {
+      pl.bit_off.push_back(pl.bit_words);
+      pl.bit_words += 2 * ((static_cast<uint64_t>(h.b) + 31) / 32);
+    }
+    if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * pl.bit_words));
+    if (!hr.empty()) {
+      NTCB_CUDA(cudaMalloc(&pl.first, sizeof(HeavyRow) * (hr.size() + 1)));
+      NTCB_CUDA(cudaMemcpy(pl.first, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
+    }
+    it = g_heavy.emplace(key, std::move(pl)).first;
   }
   const uint32_t nh = it->second.second;
   if (nh == 0) return 0;
@@ -858,12 +974,48 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   };
   const dim3 gz(gx(maxn), nh), gd(gx((maxn + 1) / 2), nh), gt(gx((maxn + 1) / 2 / kTailIlp), nh), gh(gx((maxn + 1) / 2), nh);
   k_heavy_zero<<<gz, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
-  k_heavy_draw<<<gd, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
-  k_heavy_tail<<<gt, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
-  k_heavy_head<<<gh, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  const uint32_t n_reg = it->second.n_reg;
+  int launches = 2;  // zero, exact
+  if (n_reg) {
+    const dim3 gr(gd.x, n_reg);
+    k_heavy_draw<<<gr, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
+    ++launches;
+  }
+  const HeavyPlan& hp = it->second;
+  if (hp.bit_words) NTCB_CUDA(cudaMemsetAsync(hp.bits, 0, sizeof(uint32_t) * hp.bit_words, stream));
+  for (size_t i = 0; i < hp.giant.size(); ++i) {
+    const HeavyRow& h = hp.giant[i];
+    const uint32_t W = heavy_window();
+    for (uint64_t w0 = 0; w0 < h.n; w0 += W) {
+      const uint64_t w1 = std::min<uint64_t>(h.n, w0 + W);
+      const uint64_t jend = std::min<uint64_t>(h.b, w1);
+      const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+          1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (jend + 256 * per - 1) / (256 * per))));
+      k_heavy_draw_win<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->perm_scratch, ctx->heavy_flags + n_reg + i, root,
+                                              direct, static_cast<uint32_t>(w0), static_cast<uint32_t>(w1),
+                                              hp.bits + hp.bit_off[i]);
+      ++launches;
+    }
+  }
+  if (n_reg) {
+    k_heavy_tail<<<dim3(gt.x, n_reg), 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+    k_heavy_head<<<dim3(gh.x, n_reg), 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+    launches += 2;
+  }
+  for (size_t i = 0; i < hp.giant.size(); ++i) {  // one slice per launch: its bitmaps stay in L2
+    const HeavyRow& h = hp.giant[i];
+    const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (h.n / 2 + 256 * per - 1) / (256 * per))));
+    const uint32_t* tb = hp.bits + hp.bit_off[i];
+    uint32_t* rb = hp.bits + hp.bit_off[i] + (static_cast<uint64_t>(h.b) + 31) / 32;
+    k_heavy_tail_big<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->perm_scratch, ctx->heavy_flags + n_reg + i, mask,
+                                            tb, rb);
+    k_heavy_head_big<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->heavy_flags + n_reg + i, mask, rb);
+    launches += 2;
+  }
   k_heavy_exact<<<nh, 32, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask, root, direct);
   NTCB_CUDA(cudaGetLastError());
-  return 5;
+  return launches;
 }
 
 void drop_heavy(ntcb_context* ctx) {
@@ -873,6 +1025,7 @@ void drop_heavy(ntcb_context* ctx) {
       if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
     if (mine) {
       if (it->second.first) cudaFree(it->second.first);
+      if (it->second.bits) cudaFree(it->second.bits);
       it = g_heavy.erase(it);
     } else {
       ++it;

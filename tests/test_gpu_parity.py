@@ -675,3 +675,42 @@ def test_full_scale_properties(ntc, orc, cid):
     finally:
         ctx.close()
         gc.collect()
+
+
+_WINDOWED = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle as O, paper_2109_09534_b200 as P
+orc = O.Oracle()
+lens = (300000, 131073, 65537, 90000, 5000)
+rng = np.random.default_rng(11)
+width = max(lens)
+idx = np.concatenate([np.stack([np.full(n, p), np.sort(rng.choice(width, n, replace=False))], 1)
+                      for p, n in enumerate(lens)]).astype(np.uint32)
+c = P.Context(0)
+c.load([len(lens), width], idx, np.ones(len(idx), np.float32))
+off = c.view_offsets(0)
+for cf in (0.5, 0.93, 0.02):
+    st = 0xD1CE + int(cf * 100)
+    e0, bits = c.sample_mask(0, cf, st, 2)
+    for p in range(len(lens)):
+        n = int(off[p + 1] - off[p])
+        want = np.zeros(n, bool)
+        want[orc.sample_row(n, cf, orc.fork(orc.fork(st, 2), p))] = True
+        assert np.array_equal(bits[int(off[p]) - e0: int(off[p + 1]) - e0], want), (cf, p, n)
+print("ok")
+"""
+
+
+def test_windowed_heavy_draws_bit_exact(tmp_path):
+    """Heavy slices longer than the draw window (config 5's slices of up to
+    261M entries) run their draw phase window by window; with a 2^16-entry
+    window (NTCB_HEAVY_WIN=16) slices of 65537..300000 entries take that
+    path here, and their sampled sets equal the reference's picks."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NTCB_HEAVY_WIN="16")
+    r = subprocess.run([sys.executable, "-c", _WINDOWED, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
