@@ -883,11 +883,14 @@ __global__ void k_heavy_exact(const HeavyRow* rows, uint32_t* scratch, const int
                             nullptr, mask, h.beg, nullptr);
 }
 
+constexpr uint32_t kMidSlice = 1u << 20;
 struct HeavyPlan {
   HeavyRow* first;
   uint32_t second;  // slices
   uint64_t third;   // longest slice
   uint32_t n_reg;   // slices [0, n_reg) draw in one pass; the rest (host copies in `giant`) by windows
+  uint32_t n_small = 0;                  // [0, n_small): n <= kMidSlice; [n_small, n_reg): mid slices
+  uint64_t max_small = 0, max_mid = 0;
   std::vector<HeavyRow> giant;
   uint32_t* bits = nullptr;       // per giant slice: tb and rb bitmaps over [0, b)
   std::vector<uint64_t> bit_off;  // word offset of giant slice i's tb (rb follows)
@@ -933,12 +936,23 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     // go last: windowed draws, bitmap-assisted tail and head, one per launch
     const uint32_t big = std::min(heavy_big(), heavy_window());
     std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
+    // mid slices (> kMidSlice) after the small ones: launched with wider
+    // grids so fewer of their tables are in flight at once (L2 footprint)
+    std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= kMidSlice; });
+    std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
     HeavyPlan pl{nullptr, static_cast<uint32_t>(hr.size()), maxn, 0, {}};
     for (const HeavyRow& h : hr) {
-      if (h.n <= big)
+      if (h.n <= big) {
         ++pl.n_reg;
-      else
+        if (h.n <= kMidSlice) {
+          ++pl.n_small;
+          pl.max_small = std::max<uint64_t>(pl.max_small, h.n);
+        } else {
+          pl.max_mid = std::max<uint64_t>(pl.max_mid, h.n);
+        }
+      } else {
         pl.giant.push_back(h);
+      }
     }
     for (const HeavyRow& h : pl.giant) {
       pl.bit_off.push_back(pl.bit_words);
@@ -972,16 +986,28 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   auto gx = [&](uint64_t work) {
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
   };
-  const dim3 gz(gx(maxn), nh), gd(gx((maxn + 1) / 2), nh), gt(gx((maxn + 1) / 2 / kTailIlp), nh), gh(gx((maxn + 1) / 2), nh);
+  const dim3 gz(gx(maxn), nh);
   k_heavy_zero<<<gz, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
   const uint32_t n_reg = it->second.n_reg;
   int launches = 2;  // zero, exact
-  if (n_reg) {
-    const dim3 gr(gd.x, n_reg);
-    k_heavy_draw<<<gr, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, root, direct);
+  const HeavyPlan& hp = it->second;
+  // per size class: rows [r0, r0 + cnt), longest mx, grid cap
+  struct Cls {
+    uint32_t r0, cnt;
+    uint64_t mx;
+    uint64_t cap;
+  };
+  const Cls cls[2] = {{0, hp.n_small, hp.max_small, static_cast<uint64_t>(ctx->sm_count) * 2},
+                      {hp.n_small, n_reg - hp.n_small, hp.max_mid, static_cast<uint64_t>(ctx->sm_count) * 8}};
+  auto gxc = [&](const Cls& c, uint64_t work) {
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(c.cap, (work + 256 * per - 1) / (256 * per))));
+  };
+  for (const Cls& c : cls) {
+    if (!c.cnt) continue;
+    k_heavy_draw<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->perm_scratch,
+                                                                          ctx->heavy_flags + c.r0, root, direct);
     ++launches;
   }
-  const HeavyPlan& hp = it->second;
   if (hp.bit_words) NTCB_CUDA(cudaMemsetAsync(hp.bits, 0, sizeof(uint32_t) * hp.bit_words, stream));
   for (size_t i = 0; i < hp.giant.size(); ++i) {
     const HeavyRow& h = hp.giant[i];
@@ -997,9 +1023,12 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       ++launches;
     }
   }
-  if (n_reg) {
-    k_heavy_tail<<<dim3(gt.x, n_reg), 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
-    k_heavy_head<<<dim3(gh.x, n_reg), 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask);
+  for (const Cls& c : cls) {
+    if (!c.cnt) continue;
+    k_heavy_tail<<<dim3(gxc(c, (c.mx + 1) / 2 / kTailIlp), c.cnt), 256, 0, stream>>>(
+        d + c.r0, ctx->perm_scratch, ctx->heavy_flags + c.r0, mask);
+    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->perm_scratch,
+                                                                          ctx->heavy_flags + c.r0, mask);
     launches += 2;
   }
   for (size_t i = 0; i < hp.giant.size(); ++i) {  // one slice per launch: its bitmaps stay in L2
