@@ -146,12 +146,33 @@ __device__ __forceinline__ void block_of(int blk, int nb4, int& bi, int& bj) {
 
 // Warp-level finalisation of one row from Hf (R x HS, fp32 sums of k k^T,
 // full symmetric) and g (fp64 sums of s k, in gd).  Writes A[p], Y[p].
+template <bool PRE = false>
 __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv,
-                             int lane) {
+                             int lane, float y_pre = 0.f, float a_pre = 0.f) {
   const int R = a.rank;
   const int HS = R | 1;
   const int ld = a.ld;
   const double lam = a.lambda;
+  if constexpr (PRE) {
+    // Y and A of the row were copied into shared memory with the item's
+    // first batch (R <= 32, lane r holds element r): no global round trip
+    // on the row-end latency chain (rows of a few hundred entries)
+    if (lane < R) vv[lane] = static_cast<double>(y_pre);
+    __syncwarp();
+    bool bad = false;
+    if (lane < R) {
+      const float* hr = Hf + lane * HS;
+      double hy = 0.0;
+      for (int q = 0; q < R; ++q) hy += static_cast<double>(hr[q]) * vv[q];
+      gd[lane] = hy - gd[lane] + lam * static_cast<double>(y_pre);
+      bad = !isfinite(gd[lane]);
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) report(a.counters, a.mode, p, 0);  // non-finite gradient
+      return;
+    }
+  } else {
   // On entry gd holds w = sum_e x_e k_e.  grad = sum_e (y.k_e - x_e) k_e + lambda y
   // = H y - w + lambda y with H = sum k k^T (nmc.cpp:84-105).  Forming it here
   // in fp64 instead of per pick is exact in real arithmetic; the fp32 error of
@@ -170,6 +191,7 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
   if (__any_sync(0xffffffffu, bad)) {
     if (lane == 0) report(a.counters, a.mode, p, 0);  // non-finite gradient
     return;
+  }
   }
   bool hbad = false;
   for (int i = lane; i < R * R; i += 32) hbad |= !isfinite(Hf[(i / R) * HS + (i % R)]);
@@ -230,8 +252,8 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
   const double sl = sqrt(L), sm = sqrt(lam);
   const double beta = (sl - sm) / (sl + sm);
   for (int r = lane; r < R; r += 32) {
-    const double y = static_cast<double>(a.Y[p * ld + r]);
-    const double ap = static_cast<double>(a.A[p * ld + r]);
+    const double y = static_cast<double>(PRE ? y_pre : a.Y[p * ld + r]);
+    const double ap = static_cast<double>(PRE ? a_pre : a.A[p * ld + r]);
     const double av = y - inv_l * gd[r];
     const double an = av > 0.0 ? av : 0.0;
     a.A[p * ld + r] = static_cast<float>(an);
@@ -634,8 +656,9 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
 }
 constexpr int kKtStride = 36;          // natural layout: k' tile row stride (floats, bank-skewed)
 constexpr int kKtWords = 8 * kKtStride;  // 8 picks
-__host__ __device__ constexpr int tc_words(int no, int R, bool nat = false) {
-  return tc_ring_words(no, R) + WarpSmem<1>::batch_words(no) + (nat ? kKtWords : 0);
+constexpr int kPreWords = 128;  // SHORT: [2 item parities][Y, A][32], the row's A and Y for the row end
+__host__ __device__ constexpr int tc_words(int no, int R, bool nat = false, bool shrt = false) {
+  return tc_ring_words(no, R) + WarpSmem<1>::batch_words(no) + (nat ? kKtWords : 0) + (shrt ? kPreWords : 0);
 }
 
 // base + row * ld4 bytes as one wide multiply-add
@@ -651,7 +674,7 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
 // Khatri-Rao rows k go through an 8 x 32 shared tile into the fragment
 // layout; w = sum x k is accumulated on the CUDA cores in the natural
 // layout (no x column in the tiles, so 32 features fit 4 blocks).
-template <int P, int NO, bool NAT = false>
+template <int P, int NO, bool NAT = false, bool SHORT = false>
 __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
@@ -663,7 +686,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
   const int R = a.rank;
   const int HS = R | 1;
   const int ld = a.ld;
-  float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R, NAT);
+  float* wbase = smem_f + static_cast<size_t>(wid) * tc_words(no, R, NAT, SHORT);
   float* kt = wbase + tc_ring_words(no, R) + W::batch_words(no);  // NAT: [8][kKtStride]
   uint32_t* st_o = reinterpret_cast<uint32_t*>(wbase);  // [no][kStage]
   float* st_x = wbase + no * W::kStage;                 // [kStage]
@@ -730,9 +753,21 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     if (lane == 0) it = atomicAdd(&a.counters[2], 1ull);
     return it;  // lane 0 only; broadcast when needed
   };
+  // SHORT (modes of short rows): A and Y of an item's row are copied into
+  // pre[parity] with its first batch, for the row-end finalisation
+  float* pre = wbase + tc_ring_words(no, R) + W::batch_words(no) + (NAT ? kKtWords : 0);
+  int parity = 0;
   auto begin_item = [&](unsigned long long it, WorkItem& w) {
     if (it >= a.n_items) return false;
     w = a.items[it];
+    if constexpr (SHORT) {
+      if (w.slot < 0 && lane < R) {
+        const uint64_t q = w.row * static_cast<uint64_t>(ld) + lane;
+        const unsigned dy = static_cast<unsigned>(__cvta_generic_to_shared(pre + parity * 64 + lane));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dy), "l"(a.Y + q));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dy + 128u), "l"(a.A + q));
+      }
+    }
     const uint64_t tb = w.e0 & ~uint64_t(31);  // 128-byte aligned: one line per quarter-warp cp.async
     fetch_async(tb, static_cast<int>(w.e1 - tb), 0, 0);
     return true;
@@ -746,6 +781,8 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     }
     const unsigned long long next_it = claim();
     const uint64_t p = w.row;
+    const float* my_pre = pre + parity * 64;  // SHORT: this item's A/Y copies
+    if constexpr (SHORT) parity ^= 1;
 
     float acc[G::NT][4];
 #pragma unroll
@@ -1043,7 +1080,10 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     }
     __syncwarp();
     if (cur.slot < 0) {
-      finalize_row(a, p, Hf, gd, vv, lane);
+      if constexpr (SHORT)
+        finalize_row<true>(a, p, Hf, gd, vv, lane, lane < R ? my_pre[lane] : 0.f, lane < R ? my_pre[32 + lane] : 0.f);
+      else
+        finalize_row(a, p, Hf, gd, vv, lane);
     } else {
       float* dst = a.partial + static_cast<uint64_t>(cur.slot) * (R * R + R);
       for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
@@ -1209,6 +1249,7 @@ struct WorkPlan {
   FinItem* d_fins = nullptr;  // [n_small small rows][n_fins - n_small big rows]
   SlotGroup* d_groups = nullptr;
   uint64_t n_items = 0, n_fins = 0, n_slots = 0, n_small = 0, n_groups = 0;
+  uint64_t n_entries = 0;  // entries over all items
 };
 static std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan> g_plans;
 
@@ -1253,6 +1294,7 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   pl.n_small = static_cast<uint64_t>(
       std::count_if(fins.begin(), fins.end(), [](const FinItem& f) { return f.nslots <= kFinSmall; }));
   pl.n_slots = static_cast<uint64_t>(slot);
+  for (const WorkItem& it : items) pl.n_entries += it.e1 - it.e0;
   std::vector<SlotGroup> groups;
   for (auto& f : fins) {
     if (f.nslots <= kFinSmall) continue;
@@ -1311,7 +1353,7 @@ static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, si
   return 1;
 }
 
-template <int P, int NO, bool NAT = false>
+template <int P, int NO, bool NAT = false, bool SHORT = false>
 static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
   // Few items (a small tensor or a thin row shard): fewer warps per CTA so the
   // items spread over every SM instead of filling a few.
@@ -1325,15 +1367,15 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
   }();
   const int wpc = static_cast<int>(std::min<uint64_t>(wmax, std::max<uint64_t>(1, per_sm_items)));
   smem = warp_bytes * wpc;
-  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT>, wpc * 32, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT, SHORT>, wpc * 32, smem));
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (pl.n_items + wpc - 1) / wpc;
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   grid = std::max<uint64_t>(grid, 1);
-  k_update_tc<P, NO, NAT><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
+  k_update_tc<P, NO, NAT, SHORT><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
   return 1;
 }
@@ -1363,11 +1405,19 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // per SM the pair-layout gathers of three factors measured 21 ms vs 17.6 ms
   // per mode on config 4
   static const bool nat_off = std::getenv("NTCB_NO_NAT") != nullptr;  // A/B switch
+  // rows of fewer than kShortRow entries on average: per-row latencies dominate
+  static const uint64_t short_row = [] { const char* e = std::getenv("NTCB_SHORT_ROW"); return e ? std::atoll(e) : 2048ll; }();
+  const bool short_rows = pl.n_items && pl.n_entries < short_row * pl.n_items;
   if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && a.rank >= 25 && (a.no == 2 || a.no == 3)) {
     // ranks 25-32: natural-layout gathers through a shared tile into the
     // tensor-core Gram (w on the CUDA cores)
     const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true)) * 4 * kWarps;
     launches += a.no == 2 ? launch_items_tc<4, 2, true>(ctx, a, pl, ts) : launch_items_tc<4, 3, true>(ctx, a, pl, ts);
+  } else if (pl.n_items && short_rows && a.no == 2 && (P == 2 || P == 3) && !g_tc_off) {
+    // order 3, ranks 8-23, short rows on average (Zipf tails: configs 3 and
+    // 5): the variant that stages each row's A and Y with its first batch
+    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, false, true)) * 4 * kWarps;
+    launches += P == 2 ? launch_items_tc<2, 2, false, true>(ctx, a, pl, ts) : launch_items_tc<3, 2, false, true>(ctx, a, pl, ts);
   } else if (pl.n_items && a.rank <= 31 && a.no <= 3 && !g_tc_off) {  // orders 2 to 4
     const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank)) * 4 * kWarps;
     launches += P == 1 ? launch_tc<1>(ctx, a, pl, ts)
