@@ -720,6 +720,8 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
     ub1[m] = a.U[m < no ? m : 0] + 16 * NP + g;
   }
 
+  uint64_t stream_policy = 0;
+  if constexpr (SHORT) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_policy));
   // Record batches of an item: 128 entries from tb + t into buffer buf
   // (cp.async 16-byte copies of oth[.] and val, the mask word; one group).
   auto fetch_async = [&](uint64_t tb, int hi, int t, int buf) {
@@ -733,7 +735,15 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
           const void* src = (m == NO) ? static_cast<const void*>(a.val + e) : static_cast<const void*>(a.oth[m] + e);
           const unsigned dst = static_cast<unsigned>(
               __cvta_generic_to_shared(rbat + (buf * (no + 1) + row) * 128 + 4 * lane));
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+          if constexpr (SHORT) {
+            // the view stream is read once: evict-first in L2, so it does not
+            // push out the factor rows the gathers reuse (config 5's factors
+            // exceed L2 and compete with 20 GB of streamed records per mode)
+            asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                         "l"(stream_policy));
+          } else {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+          }
         }
       }
       // one mask word per 32 entries: lanes 8i copy word i (the other lanes
@@ -859,6 +869,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
                 r.f[m][q][2 * i + 1] = v.y;
               }
               if (P & 1) r.f[m][q][P - 1] = __ldg(row_ptr(ub1[m], rw[q], ld4));
+              }
             }
           }
         }
