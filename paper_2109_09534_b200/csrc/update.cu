@@ -869,7 +869,6 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
                 r.f[m][q][2 * i + 1] = v.y;
               }
               if (P & 1) r.f[m][q][P - 1] = __ldg(row_ptr(ub1[m], rw[q], ld4));
-              }
             }
           }
         }
