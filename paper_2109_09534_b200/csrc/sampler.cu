@@ -885,9 +885,9 @@ __global__ void k_heavy_exact(const HeavyRow* rows, uint32_t* scratch, const int
 
 constexpr uint32_t kMidSlice = 1u << 20;
 struct HeavyPlan {
-  HeavyRow* first;
-  uint32_t second;  // slices
-  uint64_t third;   // longest slice
+  HeavyRow* rows;   // device copy of the slice list (order below)
+  uint32_t n;       // slices
+  uint64_t maxn;    // longest slice
   uint32_t n_reg;   // slices [0, n_reg) draw in one pass; the rest (host copies in `giant`) by windows
   uint32_t n_small = 0;                  // [0, n_small): n <= kMidSlice; [n_small, n_reg): mid slices
   uint64_t max_small = 0, max_mid = 0;
@@ -932,13 +932,12 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
         maxn = std::max<uint32_t>(maxn, static_cast<uint32_t>(n));
       }
     }
-    // slices whose table is too long to stay in L2 alongside its neighbours
-    // go last: windowed draws, bitmap-assisted tail and head, one per launch
+    // order: small slices, then mid slices (> kMidSlice: launched with wider
+    // grids so fewer of their tables are in flight at once, L2 footprint),
+    // then slices whose table is too long to stay in L2 alongside its
+    // neighbours (windowed draws, bitmap-assisted tail and head, one per launch)
     const uint32_t big = std::min(heavy_big(), heavy_window());
-    std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
-    // mid slices (> kMidSlice) after the small ones: launched with wider
-    // grids so fewer of their tables are in flight at once (L2 footprint)
-    std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= kMidSlice; });
+    std::stable_partition(hr.begin(), hr.end(), [](const HeavyRow& h) { return h.n <= kMidSlice; });
     std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
     HeavyPlan pl{nullptr, static_cast<uint32_t>(hr.size()), maxn, 0, {}};
     for (const HeavyRow& h : hr) {
@@ -960,12 +959,12 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     }
     if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * pl.bit_words));
     if (!hr.empty()) {
-      NTCB_CUDA(cudaMalloc(&pl.first, sizeof(HeavyRow) * (hr.size() + 1)));
-      NTCB_CUDA(cudaMemcpy(pl.first, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
+      NTCB_CUDA(cudaMalloc(&pl.rows, sizeof(HeavyRow) * (hr.size() + 1)));
+      NTCB_CUDA(cudaMemcpy(pl.rows, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
     }
     it = g_heavy.emplace(key, std::move(pl)).first;
   }
-  const uint32_t nh = it->second.second;
+  const uint32_t nh = it->second.n;
   if (nh == 0) return 0;
   if (nh > 65535) fail(NTCB_EINVAL, "sampler: more than 65535 heavy slices in one call");
   if (!ctx->perm_scratch) fail(NTCB_ECUDA, "sampler: heavy slices need the per-entry scratch");
@@ -974,7 +973,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     NTCB_CUDA(cudaMalloc(&ctx->heavy_flags, sizeof(int) * nh));
     ctx->heavy_flags_n = nh;
   }
-  const HeavyRow* d = it->second.first;
+  const HeavyRow* d = it->second.rows;
   // (chunk, slice) grids: 2 x SMs CTAs per slice at most, fewer when the
   // longest slice gives each thread less than ~kPer entries -- slices of a
   // few hundred thousand entries otherwise launch ~300 mostly idle CTAs
@@ -982,7 +981,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   // best: config 4 tail phase 5.06 -> 2.40 ms per mode).
   // NTCB_HEAVY_PER overrides kPer for experiments.
   static const uint64_t per = [] { const char* e = std::getenv("NTCB_HEAVY_PER"); return e ? std::max(1, std::atoi(e)) : 8; }();
-  const uint64_t maxn = it->second.third;
+  const uint64_t maxn = it->second.maxn;
   auto gx = [&](uint64_t work) {
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
   };
@@ -1053,7 +1052,7 @@ void drop_heavy(ntcb_context* ctx) {
     for (int m = 0; m < NTCB_MAX_ORDER; ++m)
       if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
     if (mine) {
-      if (it->second.first) cudaFree(it->second.first);
+      if (it->second.rows) cudaFree(it->second.rows);
       if (it->second.bits) cudaFree(it->second.bits);
       it = g_heavy.erase(it);
     } else {
