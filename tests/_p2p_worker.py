@@ -10,19 +10,28 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-DIMS, NNZ, R, SWEEPS, SEED = [300, 200, 100], 200_000, 8, 3, 11
+SWEEPS, SEED = 3, 11
+# uniform: short rows only; zipf: Zipf(1.2) modes with slices beyond the
+# sampler's shared-memory budget (heavy grid path) split into many segments
+# (slot groups), R = 16 (SHORT instantiation)
+CASES = {
+    "uniform": dict(dims=[300, 200, 100], nnz=200_000, R=8, synth=(4, 0.01, 4321, None, 0)),
+    "zipf": dict(dims=[5000, 400, 60], nnz=400_000, R=16, synth=(6, 0.5, 77, [1.2, 1.2, 0.0], 1)),
+}
 
 
-def build(P):
+def build(P, case="uniform"):
+    c = CASES[case]
     ctx = P.Context(0)
-    ctx.synth(DIMS, NNZ, 4, 0.01, 4321)
-    ctx.random_factors(R, 7)
+    tr, sigma, seed, zipf, kind = c["synth"]
+    ctx.synth(c["dims"], c["nnz"], tr, sigma, seed, zipf, kind)
+    ctx.random_factors(c["R"], 7)
     return ctx
 
 
-def run_serial():
+def run_serial(case="uniform"):
     import paper_2109_09534_b200 as P
-    ctx = build(P)
+    ctx = build(P, case)
     cfg = P.NmcConfig(c=0.5)
     for k in range(SWEEPS):
         ctx.sweep_async(k, cfg, SEED)
@@ -30,13 +39,13 @@ def run_serial():
     return [ctx.get_factor(m)[0] for m in range(3)]
 
 
-def worker(rank, world, port, out_dir):
+def worker(rank, world, port, out_dir, case="uniform"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2109_09534_b200 as P
     from paper_2109_09534_b200.dist import ShardedSweep
-    ctx = build(P)
+    ctx = build(P, case)
     sh = ShardedSweep(ctx, P.NmcConfig(c=0.5), rank, world, exchange="p2p")
     assert sh.exchange == "p2p", "peer mapping failed"
     for k in range(SWEEPS):

@@ -2,7 +2,10 @@
 update kernel into the peer replicas (CUDA IPC) -- reproduces the
 single-process sweep bit for bit on every rank.  Two processes on one GPU
 (the box has one): the mapping, the kernel-side peer stores and the barrier
-protocol are the multi-GPU ones; only the NVLink hop is missing."""
+protocol are the multi-GPU ones; only the NVLink hop is missing.  Cases: a
+uniform tensor at 2 ranks, and a Zipf tensor (heavy slices, rows cut into
+many segments and summed through slot groups, the SHORT kernel) at 2 and 3
+ranks."""
 import socket
 
 import numpy as np
@@ -18,12 +21,12 @@ def _port():
 
 
 @pytest.mark.gpu
-def test_fused_exchange_equals_serial(tmp_path, cuda_ok):
+@pytest.mark.parametrize("case,world", [("uniform", 2), ("zipf", 2), ("zipf", 3)])
+def test_fused_exchange_equals_serial(tmp_path, cuda_ok, case, world):
     import torch.multiprocessing as mp
     import _p2p_worker as W
-    world = 2
-    mp.spawn(W.worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
-    want = W.run_serial()
+    mp.spawn(W.worker, args=(world, _port(), str(tmp_path), case), nprocs=world, join=True)
+    want = W.run_serial(case)
     for r in range(world):
         got = np.load(tmp_path / f"rank{r}.npz")
         for m in range(3):
