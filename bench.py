@@ -335,6 +335,8 @@ def run_ours(args, cfgd, cid):
             tj = json.load(f)
         traffic = tj.get("dram_bytes_per_launch")
         limiter.update({k: tj.get(k) for k in ("util", "dram_util", "source") if k in tj})
+        if tj.get("limiter_unit"):
+            limiter["unit"] = tj["limiter_unit"]
 
     # ---- end to end through the host-buffer C-ABI --------------------------------
     e2e = None
