@@ -714,3 +714,48 @@ def test_windowed_heavy_draws_bit_exact(tmp_path):
     r = subprocess.run([sys.executable, "-c", _WINDOWED, root], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_subproblem_minimizer_c1(ntc):
+    """test_nmc.cpp:396-411 on the device: at c = 1 with many inner
+    iterations, every row of the mode-0 factor converges to the minimiser of
+    its nonnegative ridge subproblem min_a 1/2 sum_e (x_e - a.k_e)^2 +
+    lambda/2 |a|^2, a >= 0 (solved independently by scipy's NNLS on
+    [K; sqrt(lambda) I] a ~ [x; 0])."""
+    from scipy.optimize import nnls
+    import paper_2109_09534_b200 as P
+    dims, R, lam = [40, 30, 20], 4, 1e-2
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, 4000, 3, 0.05, 31)
+    ctx.random_factors(R, 9)
+    ci, cv = ctx.canonical()
+    ci = ci.reshape(-1, 3)
+    B, C = ctx.get_factor(1)[0].astype(np.float64), ctx.get_factor(2)[0].astype(np.float64)
+    ctx.s_nmc(0, P.NmcConfig(lambda_=lam, c=1.0, max_inner=3000), 5)
+    A = ctx.get_factor(0)[0]
+    worst = 0.0
+    for p in range(dims[0]):
+        sel = ci[:, 0] == p
+        K = B[ci[sel, 1]] * C[ci[sel, 2]]
+        x = cv[sel].astype(np.float64)
+        a_star, _ = nnls(np.vstack([K, np.sqrt(lam) * np.eye(R)]), np.concatenate([x, np.zeros(R)]))
+        worst = max(worst, np.linalg.norm(A[p] - a_star) / max(np.linalg.norm(a_star), 1e-12))
+    assert worst <= 1e-4, worst
+
+
+def test_ao_monotone_objective_c1(ntc):
+    """test_ao.cpp:294-317: with full batches (c = 1) every AO sweep does not
+    increase the objective (up to fp32 rounding of the device sums)."""
+    rng = np.random.default_rng(17)
+    dims = [25, 20, 15]
+    cells = rng.choice(int(np.prod(dims)), 2500, replace=False)
+    idx = np.stack(np.unravel_index(cells, dims), 1).astype(np.uint32)
+    vals = rng.random(len(idx)) * 3.0
+    t = ntc.SparseTensor(dims, idx, vals)
+    init = ntc.initial_factors(dims, 4, 13)
+    res = ntc.ao_ntc(t, init, ntc.AoConfig(rank=4, c=1.0, max_epochs=30.0, seed=5))
+    obj = [r.objective for r in res.history]
+    assert len(obj) >= 10
+    for a, b in zip(obj, obj[1:]):
+        assert b <= a * (1 + 1e-6), (a, b)
+    assert obj[-1] < 0.5 * obj[0]
