@@ -759,3 +759,20 @@ def test_ao_monotone_objective_c1(ntc):
     for a, b in zip(obj, obj[1:]):
         assert b <= a * (1 + 1e-6), (a, b)
     assert obj[-1] < 0.5 * obj[0]
+
+
+@pytest.mark.parametrize("c", [0.25, 0.5, 0.75])
+def test_epoch_accounting_dense(ntc, c):
+    """acceptance.cpp:475-513 (AC11): on a dense 4x4x4 tensor every slice has
+    16 entries, so a sweep accesses exactly N c nnz -- epochs advance by 3 c
+    per sweep, entries_accessed by 3 * 16 * 4 * floor(16 c) / 16."""
+    dims = [4, 4, 4]
+    idx = np.stack(np.unravel_index(np.arange(64), dims), 1).astype(np.uint32)
+    vals = np.random.default_rng(3).random(64) + 0.5
+    t = ntc.SparseTensor(dims, idx, vals)
+    init = ntc.initial_factors(dims, 2, 7)
+    res = ntc.ao_ntc(t, init, ntc.AoConfig(rank=2, c=c, max_epochs=3 * c * 5, seed=2))
+    for k, r in enumerate(res.history):
+        assert r.epoch == pytest.approx(3 * c * k, abs=1e-12)
+        assert r.entries_accessed == 3 * 4 * int(np.floor(16 * c)) * k
+    assert len(res.history) == 6
