@@ -776,3 +776,37 @@ def test_epoch_accounting_dense(ntc, c):
         assert r.epoch == pytest.approx(3 * c * k, abs=1e-12)
         assert r.entries_accessed == 3 * 4 * int(np.floor(16 * c)) * k
     assert len(res.history) == 6
+
+
+def test_cfg1_full_trajectory_vs_oracle(ntc, orc):
+    """BASELINE configs[0] exactly as bench.py generates it (500^3, 1.25M
+    observed, truth rank 10, fit rank 10, c = 0.5, 20 AO iterations): device
+    fp32 vs the fp64 restatement (bit-identical to the compiled reference),
+    same seeds.  entries_accessed exact every iteration; factors within 1e-4
+    relative every iteration; relative error (= RMSE * sqrt(nnz) / |x|) at
+    the end within 1e-5."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [500, 500, 500], 1_250_000, 10
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, nnz, 10, 0.01, 1001)
+    ci, cv = ctx.canonical()
+    cv64 = cv.astype(np.float64)
+    views = [orc.build_view(dims, ci, cv64, m) for m in range(3)]
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 7)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
+    ocfg = O.nmc_cfg(lambda_=1e-3, c=0.5, max_inner=1, threads=os.cpu_count() or 1)
+    worst = 0.0
+    for k in range(20):
+        ctx.sweep_async(k, cfg, 7)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None, ocfg, orc.sweep_state(7, k, m))
+                   for m in range(3))
+        assert acc == oacc, k
+        err = max(rel(ctx.get_factor(m)[0], F[m]) for m in range(3))
+        worst = max(worst, err)
+        assert err <= TOL, (k, err)
+    sse, den, _ = orc.metrics(dims, R, F, ci, cv64)
+    assert abs(ctx.relative_error() - np.sqrt(sse / den)) <= 1e-5 * np.sqrt(sse / den)
+    print(f"cfg1 20-iteration trajectory: worst per-iteration factor error {worst:.2e}")
