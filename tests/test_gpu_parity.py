@@ -810,3 +810,38 @@ def test_cfg1_full_trajectory_vs_oracle(ntc, orc):
     sse, den, _ = orc.metrics(dims, R, F, ci, cv64)
     assert abs(ctx.relative_error() - np.sqrt(sse / den)) <= 1e-5 * np.sqrt(sse / den)
     print(f"cfg1 20-iteration trajectory: worst per-iteration factor error {worst:.2e}")
+
+
+def test_cfg2_full_run_vs_oracle(ntc, orc):
+    """The bench workload itself, run as BASELINE configs[1] states it
+    (10^4 x 10^4 x 10^4, 10^8 observed, rank 20, c = 0.5, 10 AO iterations):
+    the device vs the fp64 restatement on the host cores, same seeds --
+    entries exact and factors within 1e-4 relative every iteration, the
+    final relative error within 1e-5."""
+    import paper_2109_09534_b200 as P
+    dims, nnz, R = [10000, 10000, 10000], 100_000_000, 20
+    ctx = P.Context(0)
+    ctx.synth_uniform(dims, nnz, 20, 0.01, 1002)
+    ci, cv = ctx.canonical()
+    cv64 = cv.astype(np.float64)
+    views = [orc.build_view(dims, ci, cv64, m) for m in range(3)]
+    del ci
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 7)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
+    ocfg = O.nmc_cfg(lambda_=1e-3, c=0.5, max_inner=1, threads=os.cpu_count() or 1)
+    worst = 0.0
+    for k in range(10):
+        ctx.sweep_async(k, cfg, 7)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None, ocfg, orc.sweep_state(7, k, m))
+                   for m in range(3))
+        assert acc == oacc, k
+        err = max(rel(ctx.get_factor(m)[0], F[m]) for m in range(3))
+        worst = max(worst, err)
+        assert err <= TOL, (k, err)
+    ci, _ = ctx.canonical()
+    sse, den, _ = orc.metrics(dims, R, F, ci, cv64)
+    assert abs(ctx.relative_error() - np.sqrt(sse / den)) <= 1e-5 * np.sqrt(sse / den)
+    print(f"cfg2 10-iteration run: worst per-iteration factor error {worst:.2e}")
