@@ -953,10 +953,21 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
         const uint32_t a0 = hb[0][m0], a2 = hb[1][m0];
         const uint32_t a1 = m1 < P ? hb[0][m1 < P ? m1 : 0] : 0u;
         const uint32_t a3 = m1 < P ? hb[1][m1 < P ? m1 : 0] : 0u;
-        mma_tf32(acc[tl], a0, a1, a2, a3, hb[0][j], hb[1][j]);
         const uint32_t c1 = m1 < P ? hp[m1 < P ? m1 : 0] : 0u;
         const uint32_t c3 = m1 < P ? lp[m1 < P ? m1 : 0] : 0u;
-        mma_bf16(acc[tl], hp[m0], c1, lp[m0], c3, lp[j], hp[j]);
+        // The MMA's fp32 accumulation does not round to nearest: accumulating
+        // a whole item (thousands of groups) in its C registers leaves a
+        // signed error that grows with the number of groups (measured 7e-5
+        // relative on config 4's NAT mode updates, whose w is summed on the
+        // CUDA cores, and 3.4e-5 on config 3's mode 2, where the bias only
+        // partly cancels between H and the x column).  So each group's
+        // products are formed from zero and added to the running sums with
+        // round-to-nearest FADDs: ~3e-7 everywhere, for +2.4 % on config 2.
+        float t4[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_tf32(t4, a0, a1, a2, a3, hb[0][j], hb[1][j]);
+        mma_bf16(t4, hp[m0], c1, lp[m0], c3, lp[j], hp[j]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[tl][e] += t4[e];
       }
     };
     // all staged full groups, three-way rotation (two gathers in flight)

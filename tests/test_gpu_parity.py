@@ -845,3 +845,35 @@ def test_cfg2_full_run_vs_oracle(ntc, orc):
     sse, den, _ = orc.metrics(dims, R, F, ci, cv64)
     assert abs(ctx.relative_error() - np.sqrt(sse / den)) <= 1e-5 * np.sqrt(sse / den)
     print(f"cfg2 10-iteration run: worst per-iteration factor error {worst:.2e}")
+
+
+@pytest.mark.parametrize("cid,iters", [(3, 2), (4, 1)])
+def test_full_size_iterations_vs_oracle(ntc, orc, cid, iters):
+    """Configs 3 (Zipf ratings, slices up to 9M entries: heavy sampler, split
+    rows, slot groups) and 4 (4-way, rank 32, NAT update) at their full
+    BASELINE sizes: AO iterations on the device vs the fp64 restatement,
+    same seeds -- entries exact, factors within 1e-4 relative."""
+    import paper_2109_09534_b200 as P
+    c = _FULL[cid]
+    dims, R = c["dims"], c["R"]
+    N = len(dims)
+    ctx = P.Context(0)
+    ctx.synth(dims, c["nnz"], c["true_rank"], c["sigma"], 1000 + cid, c.get("zipf"), c.get("kind", 0))
+    ci, cv = ctx.canonical()
+    cv64 = cv.astype(np.float64)
+    views = [orc.build_view(dims, ci, cv64, m) for m in range(N)]
+    del ci, cv
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 7)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
+    ocfg = O.nmc_cfg(lambda_=1e-3, c=0.5, max_inner=1, threads=os.cpu_count() or 1)
+    for k in range(iters):
+        ctx.sweep_async(k, cfg, 7)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None, ocfg, orc.sweep_state(7, k, m))
+                   for m in range(N))
+        assert acc == oacc, k
+        err = max(rel(ctx.get_factor(m)[0], F[m]) for m in range(N))
+        assert err <= TOL, (k, err)
+        print(f"cfg{cid} iteration {k}: factor error {err:.2e}")
