@@ -10,5 +10,5 @@ for c in 1 3 4 5; do python bench.py --config $c --no-cpu --steps 5 > gpurun_out
 NTCB_FORCE_SHARDED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --no-cpu --steps 5 > gpurun_out/bench2_sharded.json 2> gpurun_out/bench2_sharded.err
 for c in 2 3 4 5; do timeout 600 python tools/shard_probe.py --config $c > gpurun_out/shard_cfg$c.txt 2>&1; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches2.csv python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_update_tc" -s 3 -c 1 -o gpurun_out/v18_cfg2 python bench.py --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:"k_sample_cta" -s 3 -c 1 -o gpurun_out/v18_cfg2_sampler python bench.py --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_update_tc" -s 3 -c 1 -o gpurun_out/v20_cfg2 python bench.py --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:"k_sample_cta" -s 3 -c 1 -o gpurun_out/v20_cfg2_sampler python bench.py --no-cpu --steps 1 --warmup 1 > /dev/null 2>&1
