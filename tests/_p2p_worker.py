@@ -17,6 +17,8 @@ SWEEPS, SEED = 3, 11
 CASES = {
     "uniform": dict(dims=[300, 200, 100], nnz=200_000, R=8, synth=(4, 0.01, 4321, None, 0)),
     "zipf": dict(dims=[5000, 400, 60], nnz=400_000, R=16, synth=(6, 0.5, 77, [1.2, 1.2, 0.0], 1)),
+    # order 4, rank 32: the NAT update (natural-layout gathers, shared tile)
+    "nat4": dict(dims=[60, 50, 40, 30], nnz=120_000, R=32, synth=(8, 0.01, 99, None, 0)),
 }
 
 
@@ -36,7 +38,7 @@ def run_serial(case="uniform"):
     for k in range(SWEEPS):
         ctx.sweep_async(k, cfg, SEED)
     ctx.collect()
-    return [ctx.get_factor(m)[0] for m in range(3)]
+    return [ctx.get_factor(m)[0] for m in range(len(CASES[case]["dims"]))]
 
 
 def worker(rank, world, port, out_dir, case="uniform"):
@@ -52,6 +54,6 @@ def worker(rank, world, port, out_dir, case="uniform"):
         sh.sweep(k, SEED)
     ctx.collect()
     dist.barrier()
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), *[ctx.get_factor(m)[0] for m in range(3)])
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), *[ctx.get_factor(m)[0] for m in range(len(CASES[case]["dims"]))])
     dist.barrier()
     dist.destroy_process_group()

@@ -5,7 +5,7 @@ single-process sweep bit for bit on every rank.  Two processes on one GPU
 protocol are the multi-GPU ones; only the NVLink hop is missing.  Cases: a
 uniform tensor at 2 ranks, and a Zipf tensor (heavy slices, rows cut into
 many segments and summed through slot groups, the SHORT kernel) at 2 and 3
-ranks."""
+ranks, and an order-4 rank-32 tensor (the NAT update) at 2 ranks."""
 import socket
 
 import numpy as np
@@ -21,7 +21,7 @@ def _port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("uniform", 2), ("zipf", 2), ("zipf", 3)])
+@pytest.mark.parametrize("case,world", [("uniform", 2), ("zipf", 2), ("zipf", 3), ("nat4", 2)])
 def test_fused_exchange_equals_serial(tmp_path, cuda_ok, case, world):
     import torch.multiprocessing as mp
     import _p2p_worker as W
@@ -29,5 +29,5 @@ def test_fused_exchange_equals_serial(tmp_path, cuda_ok, case, world):
     want = W.run_serial(case)
     for r in range(world):
         got = np.load(tmp_path / f"rank{r}.npz")
-        for m in range(3):
+        for m in range(len(want)):
             np.testing.assert_array_equal(got[f"arr_{m}"], want[m])
