@@ -243,6 +243,8 @@ def run_ours(args, cfgd, cid):
     dims, R = cfgd["dims"], cfgd["R"]
     order = len(dims)
     ctx = P.Context(local)
+    if args.tune:  # launch-policy A/B knobs (ntcb_tuning; results unchanged)
+        ctx.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tune)})
     ctx.set_stream(stream.cuda_stream)
     generate(ctx, cfgd, cid)
     ctx.random_factors(R, SEED_SOLVER)
@@ -451,6 +453,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--tune", nargs="*", default=[], metavar="K=V",
+                    help="ntcb_tuning launch-policy knobs for A/B runs, e.g. --tune split_rows=1")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":

@@ -95,6 +95,29 @@ int ntcb_destroy(ntcb_context* ctx);
 int ntcb_set_stream(ntcb_context* ctx, void* cuda_stream);
 int ntcb_synchronize(ntcb_context* ctx);
 
+/* ---- tuning (launch policy only; no reference analogue) -----------------
+ * Per-context launch choices behind the measured defaults of DESIGN.md §3.
+ * None of them changes results: every variant computes the same sampled
+ * sets, and the update variants the same factors (they are A/B switches for
+ * measurements, set through this struct -- never through the environment).
+ * ntcb_tuning_defaults fills the defaults; ntcb_set_tuning validates and
+ * applies (cached launch plans are rebuilt on demand). */
+typedef struct ntcb_tuning {
+  int32_t no_tc;             /* 1: CUDA-core Gram (k_update) instead of the tensor-core kernels */
+  int32_t no_nat;            /* 1: ranks 25-32 without the natural-layout (NAT) gathers */
+  int32_t tc_p;              /* 0 or 4: 4 = quad gather layout at ranks <= 31 (measured slower) */
+  int32_t update_wpc;        /* warps per CTA of k_update_tc, 1..8 (default 4) */
+  int64_t short_row;         /* average item length below which the SHORT update runs (2048) */
+  int32_t side_sampler_ctas; /* CTAs per SM of the side-stream CTA sampler, 0 = no cap */
+  int32_t heavy_per;         /* entries per thread when sizing heavy-slice sampler grids (8) */
+  int32_t heavy_win_log2;    /* log2 of the heavy sampler's draw window (24) */
+  int32_t heavy_big_log2;    /* log2 of the slice length taking the windowed path (24) */
+  int32_t host_threads;      /* host threads for fp64 <-> fp32 factor conversion, 0 = min(cores, 16) */
+} ntcb_tuning;
+void ntcb_tuning_defaults(ntcb_tuning* t);
+int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t);
+int ntcb_get_tuning(ntcb_context* ctx, ntcb_tuning* t);
+
 /* ---- RNG (rng.hpp:13-63, ao.cpp:65-68) — host-side helpers ------------- */
 uint64_t ntcb_rng_fork(uint64_t state, uint64_t tag);
 uint64_t ntcb_sweep_stream_state(uint64_t seed, uint64_t sweep, int mode);

@@ -63,6 +63,14 @@ class MetricsRecordC(C.Structure):
                 ("wall_seconds", C.c_double), ("entries_accessed", C.c_uint64)]
 
 
+class TuningC(C.Structure):
+    _fields_ = [("no_tc", C.c_int32), ("no_nat", C.c_int32), ("tc_p", C.c_int32),
+                ("update_wpc", C.c_int32), ("short_row", C.c_int64),
+                ("side_sampler_ctas", C.c_int32), ("heavy_per", C.c_int32),
+                ("heavy_win_log2", C.c_int32), ("heavy_big_log2", C.c_int32),
+                ("host_threads", C.c_int32)]
+
+
 OBSERVER = C.CFUNCTYPE(None, C.POINTER(MetricsRecordC), C.c_void_p, C.c_void_p)
 
 # name -> (restype, argtypes); every symbol declared in include/ntc_b200.h
@@ -73,6 +81,9 @@ SIGNATURES = {
     "ntcb_destroy": (C.c_int, [C.c_void_p]),
     "ntcb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ntcb_synchronize": (C.c_int, [C.c_void_p]),
+    "ntcb_tuning_defaults": (None, [C.POINTER(TuningC)]),
+    "ntcb_set_tuning": (C.c_int, [C.c_void_p, C.POINTER(TuningC)]),
+    "ntcb_get_tuning": (C.c_int, [C.c_void_p, C.POINTER(TuningC)]),
     "ntcb_rng_fork": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "ntcb_sweep_stream_state": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_int]),
     "ntcb_tensor_load": (C.c_int, [C.c_void_p, C.c_int, u64p, C.c_uint64, u32p, f64p]),

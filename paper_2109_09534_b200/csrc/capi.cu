@@ -31,6 +31,9 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
                         uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
                         uint64_t cap);
 void free_views(ntcb_context* ctx);
+void drop_plans(ntcb_context* ctx);
+void drop_heavy(ntcb_context* ctx);
+void drop_sample_plans(ntcb_context* ctx);
 void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                      const uint32_t* h_idx, const double* h_vals);
 void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
@@ -49,7 +52,7 @@ namespace {
 
 thread_local std::string g_err;
 
-// Per-context host bookkeeping that does not belong in the POD context.
+// Per-context host bookkeeping (owned by the context: ctx->host).
 struct HostState {
   uint64_t pending_accessed = 0;
   bool verified[NTCB_MAX_ORDER] = {};  // factor rows known nonnegative
@@ -58,7 +61,7 @@ struct HostState {
   uint64_t stage_n = 0;    // floats
   bool queued = false;     // work enqueued since the last collect
 };
-std::map<const ntcb_context*, HostState> g_host;
+HostState& host_of(ntcb_context* ctx) { return *static_cast<HostState*>(ctx->host); }
 
 #define API_TRY try {
 #define API_CATCH                                   \
@@ -98,7 +101,7 @@ void validate_nmc(const ntcb_nmc_config* c) {  // NmcConfig::validate, nmc.cpp:1
 
 // sum over rows of floor(c * n_p) (nmc.cpp:36-40) -- known before the run.
 uint64_t blocksize_sum(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, double c) {
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   uint64_t cbits;
   std::memcpy(&cbits, &c, 8);
   auto key = std::make_tuple(mode, r0, r1, cbits);
@@ -155,11 +158,13 @@ int enqueue_sample(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, const 
 }
 
 // presampled >= 0: the parity enqueue_sample already filled for l = 0.
-void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
-                  const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
+// Returns the entries this call will access (also added to the pending
+// count that ntcb_collect hands back).
+uint64_t enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
+                      const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
   const uint64_t ld = ctx->ld;
   cudaStream_t st = ctx->stream;
-  if (r1 <= r0) return;
+  if (r1 <= r0) return 0;
   // A_0 = Y_0 = a_init (nmc.cpp:212-215); A already holds a_init.
   NTCB_CUDA(cudaMemcpyAsync(ctx->Y[mode] + r0 * ld, ctx->A[mode] + r0 * ld,
                             sizeof(float) * (r1 - r0) * ld, cudaMemcpyDeviceToDevice, st));
@@ -178,25 +183,38 @@ void enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
     NTCB_CUDA(cudaEventRecord(ctx->ev_consumed[mode][par], st));
     ctx->consumed_valid[mode][par] = true;
   }
-  g_host[ctx].queued = true;
-  g_host[ctx].pending_accessed +=
-      static_cast<uint64_t>(cfg.max_inner) * blocksize_sum(ctx, mode, r0, r1, cfg.c);
+  host_of(ctx).queued = true;
+  const uint64_t n = static_cast<uint64_t>(cfg.max_inner) * blocksize_sum(ctx, mode, r0, r1, cfg.c);
+  host_of(ctx).pending_accessed += n;
+  return n;
+}
+
+// Work whose count the caller consumes itself (s_nmc, ao_ntc): enqueued like
+// any other, but its entries are taken out of the pending count again, so a
+// later ntcb_collect still returns exactly the async work queued by the user.
+uint64_t enqueue_snmc_owned(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
+                            const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
+  const uint64_t n = enqueue_snmc(ctx, mode, r0, r1, cfg, rng_state, presampled);
+  host_of(ctx).pending_accessed -= n;
+  return n;
 }
 
 // Waits and converts a device-side row failure into the reference's exception.
 // One host synchronisation: the main stream waits for the side stream, then
-// the error key comes back by an async copy into pinned memory.
+// the error key comes back by an async copy into pinned memory.  The pending
+// entry count (async work queued through the C-ABI) is handed back and reset
+// only when `accessed` is given: internal drains keep it for ntcb_collect.
 void collect(ntcb_context* ctx, uint64_t* accessed) {
   NTCB_CUDA(cudaEventRecord(ctx->ev_side_done, ctx->side));
   NTCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_side_done, 0));
   NTCB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 2 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, ctx->stream));
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   hs.queued = false;
   const unsigned long long key = ctx->h_counters[1];
   const uint64_t pend = hs.pending_accessed;
-  hs.pending_accessed = 0;
+  if (accessed) hs.pending_accessed = 0;
   if (key != ~0ull) {
     const unsigned long long reset = ~0ull;
     NTCB_CUDA(cudaMemcpyAsync(ctx->counters + 1, &reset, sizeof reset, cudaMemcpyHostToDevice, ctx->stream));
@@ -215,7 +233,7 @@ void collect(ntcb_context* ctx, uint64_t* accessed) {
 }
 
 float* host_stage(ntcb_context* ctx, uint64_t n) {
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   if (hs.stage_n < n) {
     if (hs.stage) cudaFreeHost(hs.stage);
     hs.stage = nullptr;
@@ -261,8 +279,7 @@ class HostPool {
  private:
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    unsigned n = std::min(hw, 16u) - 1;
-    if (const char* e = std::getenv("NTCB_HOST_THREADS")) n = std::max(1, std::atoi(e)) - 1;  // A/B knob
+    const unsigned n = std::min(hw, 16u) - 1;
     for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
     for (auto& w : workers_) w.detach();
   }
@@ -290,11 +307,14 @@ class HostPool {
   uint64_t gen_ = 0;
 };
 
-// f(row_begin, row_end) over [0, rows), split over the pool for large factors
+// f(row_begin, row_end) over [0, rows), split over the pool for large
+// factors (at most ntcb_tuning.host_threads threads when it is set)
 template <class F>
-bool parallel_rows(uint64_t rows, uint64_t per_row, F f) {
+bool parallel_rows(const ntcb_context* ctx, uint64_t rows, uint64_t per_row, F f) {
   HostPool& pool = HostPool::get();
-  const uint64_t nt = std::min<uint64_t>(pool.size(), std::max<uint64_t>(1, rows * per_row / (1 << 15)));
+  const uint64_t cap = ctx->tune.host_threads > 0 ? static_cast<uint64_t>(ctx->tune.host_threads) : pool.size();
+  const uint64_t nt = std::min<uint64_t>(std::min<uint64_t>(pool.size(), cap),
+                                         std::max<uint64_t>(1, rows * per_row / (1 << 15)));
   if (nt <= 1) return f(0, rows);
   std::vector<char> ok(nt, 1);
   const std::function<void(int)> job = [&](int t) {
@@ -309,7 +329,7 @@ bool parallel_rows(uint64_t rows, uint64_t per_row, F f) {
 bool upload_factor_async(ntcb_context* ctx, float* dst, const double* src, uint64_t rows) {
   const uint64_t R = ctx->rank, ld = ctx->ld;
   float* tmp = host_stage(ctx, rows * ld);
-  const bool ok = parallel_rows(rows, R, [&](uint64_t i0, uint64_t i1) {
+  const bool ok = parallel_rows(ctx, rows, R, [&](uint64_t i0, uint64_t i1) {
     bool good = true;
     for (uint64_t i = i0; i < i1; ++i) {
       const double* s = src + i * R;
@@ -338,8 +358,8 @@ void download_factors_enqueue(ntcb_context* ctx, int mode, bool a, bool y) {
 // staging -> host doubles (after the main stream has been synchronised)
 void download_factors_finish(ntcb_context* ctx, int mode, double* a, double* y) {
   const uint64_t R = ctx->rank, ld = ctx->ld, rows = ctx->dims[mode], n = rows * ld;
-  float* tmp = g_host[ctx].stage;
-  parallel_rows(rows, 2 * R, [&](uint64_t i0, uint64_t i1) {
+  float* tmp = host_of(ctx).stage;
+  parallel_rows(ctx, rows, 2 * R, [&](uint64_t i0, uint64_t i1) {
     for (int w = 0; w < 2; ++w) {
       double* dst = w ? y : a;
       if (!dst) continue;
@@ -411,7 +431,7 @@ void alloc_factors(ntcb_context* ctx, uint64_t rank) {
     NTCB_CUDA(cudaMemsetAsync(ctx->A[m], 0, bytes, ctx->stream));
     NTCB_CUDA(cudaMemsetAsync(ctx->Y[m], 0, bytes, ctx->stream));
   }
-  for (auto& v : g_host[ctx].verified) v = false;
+  for (auto& v : host_of(ctx).verified) v = false;
 }
 
 __global__ void k_uniform_factor(uint64_t root, uint64_t rows, int R, int ld, float* a, float* y) {
@@ -463,7 +483,7 @@ int ntcb_create(int device, ntcb_context** out) {
   const unsigned long long init[8] = {0, ~0ull, 0, 0, 0, 0, 0, 0};
   NTCB_CUDA(cudaMemcpy(ctx->counters, init, sizeof init, cudaMemcpyHostToDevice));
   for (auto& e : ctx->prof.ev) NTCB_CUDA(cudaEventCreate(&e));
-  g_host[ctx] = HostState{};
+  ctx->host = new HostState();
   *out = ctx;
   API_CATCH
 }
@@ -486,9 +506,9 @@ int ntcb_destroy(ntcb_context* ctx) {
   if (ctx->ev_side_done) cudaEventDestroy(ctx->ev_side_done);
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
-  if (g_host[ctx].stage) cudaFreeHost(g_host[ctx].stage);
+  if (host_of(ctx).stage) cudaFreeHost(host_of(ctx).stage);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
-  g_host.erase(ctx);
+  delete static_cast<HostState*>(ctx->host);
   delete ctx;
   API_CATCH
 }
@@ -507,6 +527,38 @@ int ntcb_synchronize(ntcb_context* ctx) {
   API_CATCH
 }
 
+void ntcb_tuning_defaults(ntcb_tuning* t) {
+  if (t) *t = default_tuning();
+}
+
+int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
+  API_TRY
+  need_ctx(ctx);
+  if (!t) fail(NTCB_EINVAL, "tuning: null");
+  if (t->tc_p != 0 && t->tc_p != 4) fail(NTCB_EINVAL, "tuning: tc_p must be 0 or 4");
+  if (t->update_wpc < 1 || t->update_wpc > 8) fail(NTCB_EINVAL, "tuning: update_wpc must be in [1, 8]");
+  if (t->short_row < 0) fail(NTCB_EINVAL, "tuning: short_row must be >= 0");
+  if (t->side_sampler_ctas < 0) fail(NTCB_EINVAL, "tuning: side_sampler_ctas must be >= 0");
+  if (t->heavy_per < 1) fail(NTCB_EINVAL, "tuning: heavy_per must be >= 1");
+  if (t->heavy_win_log2 < 16 || t->heavy_win_log2 > 30 || t->heavy_big_log2 < 16 || t->heavy_big_log2 > 30)
+    fail(NTCB_EINVAL, "tuning: heavy_win_log2 / heavy_big_log2 must be in [16, 30]");
+  if (t->host_threads < 0) fail(NTCB_EINVAL, "tuning: host_threads must be >= 0");
+  collect(ctx, nullptr);  // queued work keeps the plans it was launched with
+  ctx->tune = *t;
+  drop_plans(ctx);  // plans bake in the heavy-window sizes and the short-row decision
+  drop_heavy(ctx);
+  drop_sample_plans(ctx);
+  API_CATCH
+}
+
+int ntcb_get_tuning(ntcb_context* ctx, ntcb_tuning* t) {
+  API_TRY
+  need_ctx(ctx);
+  if (!t) fail(NTCB_EINVAL, "tuning: null");
+  *t = ctx->tune;
+  API_CATCH
+}
+
 uint64_t ntcb_rng_fork(uint64_t state, uint64_t tag) { return fork64(state, tag); }
 uint64_t ntcb_sweep_stream_state(uint64_t seed, uint64_t sweep, int mode) {
   return fork64(fork64(fork64(seed, 2), sweep), static_cast<uint64_t>(mode));  // ao.cpp:65-68
@@ -518,7 +570,7 @@ int ntcb_tensor_load(ntcb_context* ctx, int order, const uint64_t* dims, uint64_
   need_ctx(ctx);
   free_factors(ctx);
   load_tensor_f64(ctx, order, dims, nnz, indices, values);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -528,7 +580,7 @@ int ntcb_tensor_load_f32(ntcb_context* ctx, int order, const uint64_t* dims, uin
   need_ctx(ctx);
   free_factors(ctx);
   load_tensor_f32(ctx, order, dims, nnz, indices, values, false);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -538,7 +590,7 @@ int ntcb_tensor_load_device(ntcb_context* ctx, int order, const uint64_t* dims, 
   need_ctx(ctx);
   free_factors(ctx);
   load_tensor_f32(ctx, order, dims, nnz, d_indices, d_values, true);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -548,7 +600,7 @@ int ntcb_synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint6
   need_ctx(ctx);
   free_factors(ctx);
   synth_uniform(ctx, order, dims, nnz, true_rank, sigma, seed);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -559,7 +611,7 @@ int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
   need_ctx(ctx);
   free_factors(ctx);
   synth_general(ctx, order, dims, nnz, true_rank, sigma, seed, zipf_alpha, value_kind);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -583,7 +635,7 @@ int ntcb_tensor_read_tns(ntcb_context* ctx, const char* path) {
   } fr{idx, val};
   free_factors(ctx);
   load_tensor_f64(ctx, order, dims, nnz, idx, val);
-  g_host[ctx].bs_cache.clear();
+  host_of(ctx).bs_cache.clear();
   API_CATCH
 }
 
@@ -668,7 +720,7 @@ int ntcb_factors_init(ntcb_context* ctx, uint64_t rank, const double* const* fac
   API_TRY
   need_ctx(ctx);
   alloc_factors(ctx, rank);
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   for (int m = 0; m < ctx->order; ++m) {
     upload_factor(ctx, ctx->A[m], factors[m], ctx->dims[m]);
     upload_factor(ctx, ctx->Y[m], momentum ? momentum[m] : factors[m], ctx->dims[m]);
@@ -689,7 +741,7 @@ int ntcb_factors_random(ntcb_context* ctx, uint64_t rank, uint64_t seed) {
                                                  static_cast<int>(rank), static_cast<int>(ctx->ld),
                                                  ctx->A[m], ctx->Y[m]);
     NTCB_CUDA(cudaGetLastError());
-    g_host[ctx].verified[m] = true;
+    host_of(ctx).verified[m] = true;
   }
   NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_CATCH
@@ -702,7 +754,7 @@ int ntcb_factor_set(ntcb_context* ctx, int mode, const double* a, const double* 
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "factor_set: mode out of range");
   if (a) {
     upload_factor(ctx, ctx->A[mode], a, ctx->dims[mode]);
-    g_host[ctx].verified[mode] = all_nonneg(a, ctx->dims[mode] * ctx->rank);
+    host_of(ctx).verified[mode] = all_nonneg(a, ctx->dims[mode] * ctx->rank);
   }
   if (y) upload_factor(ctx, ctx->Y[mode], y, ctx->dims[mode]);
   API_CATCH
@@ -776,7 +828,7 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
   validate_nmc(cfg);
   need_factors(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   if (!a_init && !hs.verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   if (hs.queued) collect(ctx, nullptr);  // drain (and report) anything queued before
   int pre = -1;
@@ -791,9 +843,10 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
     }
     hs.verified[mode] = true;
   }
-  enqueue_snmc(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, pre);
+  const uint64_t own = enqueue_snmc_owned(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, pre);
   if (outs) download_factors_enqueue(ctx, mode, a_out != nullptr, y_out != nullptr);
-  collect(ctx, entries_accessed);  // the one synchronisation of the call
+  collect(ctx, nullptr);  // the one synchronisation of the call
+  if (entries_accessed) *entries_accessed += own;  // nmc.cpp:270 (+=)
   if (outs) download_factors_finish(ctx, mode, a_out, y_out);
   API_CATCH
 }
@@ -818,7 +871,7 @@ int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint6
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
   if (row_begin > row_end || row_end > ctx->dims[mode])
     fail(NTCB_ERANGE, "s_nmc: row range out of bounds");
-  if (!g_host[ctx].verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+  if (!host_of(ctx).verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   enqueue_snmc(ctx, mode, row_begin, row_end, *cfg, rng_state);
   API_CATCH
 }
@@ -929,7 +982,7 @@ int ntcb_sweep_async(ntcb_context* ctx, uint64_t sweep, const ntcb_nmc_config* c
   validate_nmc(cfg);
   need_factors(ctx);
   for (int i = 0; i < ctx->order; ++i) {
-    if (!g_host[ctx].verified[i]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+    if (!host_of(ctx).verified[i]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
     enqueue_snmc(ctx, i, 0, ctx->dims[i], *cfg, ntcb_sweep_stream_state(seed, sweep, i));
   }
   API_CATCH
@@ -996,7 +1049,7 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
   validate_nmc(&n);
   need_factors(ctx);
   if (ctx->rank != cfg->rank) fail(NTCB_EINVAL, "ao_ntc: init rank differs from configured rank");
-  auto& hs = g_host[ctx];
+  auto& hs = host_of(ctx);
   for (int m = 0; m < ctx->order; ++m)
     if (!hs.verified[m]) fail(NTCB_EINVAL, "ao_ntc: init factors must be nonnegative");
   collect(ctx, nullptr);
@@ -1031,8 +1084,8 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
     if (plateau(hist, cfg->term_tol)) break;
     uint64_t st = 0;
     for (int i = 0; i < ctx->order; ++i)
-      enqueue_snmc(ctx, i, 0, ctx->dims[i], n, ntcb_sweep_stream_state(cfg->seed, k, i));
-    collect(ctx, &st);
+      st += enqueue_snmc_owned(ctx, i, 0, ctx->dims[i], n, ntcb_sweep_stream_state(cfg->seed, k, i));
+    collect(ctx, nullptr);
     if (st == 0) break;
     accessed += st;
     last_recorded = ((k + 1) % static_cast<uint64_t>(cfg->metrics_every) == 0);

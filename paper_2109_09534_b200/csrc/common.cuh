@@ -93,6 +93,26 @@ struct Profile {
   uint64_t update_launches = 0;
 };
 
+inline ntcb_tuning default_tuning() {
+  ntcb_tuning t{};
+  t.no_tc = 0;
+  t.no_nat = 0;
+  t.tc_p = 0;
+  t.update_wpc = 4;
+  t.short_row = 2048;
+  t.side_sampler_ctas = 0;
+  t.heavy_per = 8;
+  t.heavy_win_log2 = 24;
+  t.heavy_big_log2 = 24;
+  t.host_threads = 0;
+  return t;
+}
+
+// Per-context caches of the translation units (launch plans keyed by mode,
+// row range and c).  Owned by the context, so two contexts on two host
+// threads never share a container; a context itself is not re-entrant.
+enum CacheSlot { kCacheUpdate = 0, kCacheSample, kCacheHeavy, kCacheMetrics, kCacheSlots };
+
 }  // namespace ntcb
 
 // The opaque context behind ntcb_context*.
@@ -138,6 +158,23 @@ struct ntcb_context {
   uint64_t red_n = 0;
   int error_mode = -1;    // mode of the queued updates (error text)
 
-  // synthetic data buffers (owned)
+  ntcb_tuning tune = ntcb::default_tuning();
+  void* cache[ntcb::kCacheSlots] = {};  // per-TU plan maps (see CacheSlot)
+  void* host = nullptr;                 // capi.cu host bookkeeping (HostState)
+
   ntcb::Profile prof;
 };
+
+namespace ntcb {
+// The map of cache slot k of a context, created on first use.
+template <class M>
+M& ctx_cache(ntcb_context* ctx, int k) {
+  if (!ctx->cache[k]) ctx->cache[k] = new M();
+  return *static_cast<M*>(ctx->cache[k]);
+}
+template <class M>
+void ctx_cache_free(ntcb_context* ctx, int k) {
+  delete static_cast<M*>(ctx->cache[k]);
+  ctx->cache[k] = nullptr;
+}
+}  // namespace ntcb

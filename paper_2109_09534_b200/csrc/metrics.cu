@@ -187,9 +187,10 @@ struct MPlan {
   MItem* items = nullptr;
   uint64_t n = 0;
 };
-std::map<const void*, MPlan> g_mplans;
+using MPlans = std::map<const void*, MPlan>;
 
 const MPlan& mplan(ntcb_context* ctx) {
+  auto& g_mplans = ctx_cache<MPlans>(ctx, kCacheMetrics);
   const DeviceView& v = ctx->views[0];
   auto it = g_mplans.find(v.off);
   if (it != g_mplans.end()) return it->second;
@@ -213,12 +214,10 @@ const MPlan& mplan(ntcb_context* ctx) {
 }  // namespace
 
 void drop_metric_plans(ntcb_context* ctx) {
-  for (int m = 0; m < NTCB_MAX_ORDER; ++m) {
-    auto it = g_mplans.find(ctx->views[m].off);
-    if (it == g_mplans.end()) continue;
-    if (it->second.items) cudaFree(it->second.items);
-    g_mplans.erase(it);
-  }
+  if (!ctx->cache[kCacheMetrics]) return;
+  for (auto& kv : ctx_cache<MPlans>(ctx, kCacheMetrics))
+    if (kv.second.items) cudaFree(kv.second.items);
+  ctx_cache_free<MPlans>(ctx, kCacheMetrics);
 }
 
 void device_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg) {

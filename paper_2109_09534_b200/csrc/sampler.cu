@@ -545,9 +545,11 @@ struct SamplePlan {
   uint64_t n_short = 0;
   SampleBucket mid[2];
 };
-static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, SamplePlan> g_splans;
+using SamplePlans = std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, SamplePlan>;
 
-static const SamplePlan& sample_plan(const DeviceView& v, uint64_t r0, uint64_t r1, uint64_t cap) {
+static const SamplePlan& sample_plan(ntcb_context* ctx, const DeviceView& v, uint64_t r0, uint64_t r1,
+                                     uint64_t cap) {
+  auto& g_splans = ctx_cache<SamplePlans>(ctx, kCacheSample);
   auto key = std::make_tuple(static_cast<const void*>(v.off), r0, r1, cap);
   auto it = g_splans.find(key);
   if (it != g_splans.end()) return it->second;
@@ -586,10 +588,7 @@ static void launch_cta_bucket(ntcb_context* ctx, cudaStream_t stream, const Samp
   int per_sm = 0;
   NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_cta<T>, T, smem));
   if (per_sm < 1) per_sm = 1;
-  static const int side_cap = [] {
-    const char* e = std::getenv("NTCB_SIDE_SAMPLER_CTAS");  // experiment knob
-    return e ? std::atoi(e) : 0;
-  }();
+  const int side_cap = ctx->tune.side_sampler_ctas;  // tuning knob (ntcb_tuning)
   if (stream == ctx->side && side_cap > 0) per_sm = std::min(per_sm, side_cap);
   const uint64_t grid = std::min<uint64_t>(bk.n, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   NTCB_CUDA(cudaMemsetAsync(a.cursor, 0, sizeof(unsigned long long), stream));
@@ -611,7 +610,7 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
   uint64_t cap = std::min<uint64_t>(v.max_slice, 49152);
   if (cap < kWarpCap) cap = kWarpCap;
   if (heavy_cap) *heavy_cap = cap;
-  const SamplePlan& pl = sample_plan(v, row_begin, row_end, cap);
+  const SamplePlan& pl = sample_plan(ctx, v, row_begin, row_end, cap);
   int launches = 0;
   if (pl.n_short) {
     SampleArgs a{};
@@ -657,18 +656,11 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
 }
 
 void drop_sample_plans(ntcb_context* ctx) {
-  for (auto it = g_splans.begin(); it != g_splans.end();) {
-    bool mine = false;
-    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
-      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
-    if (mine) {
-      for (auto& b : it->second.mid)
-        if (b.rows) cudaFree(b.rows);
-      it = g_splans.erase(it);
-    } else {
-      ++it;
-    }
-  }
+  if (!ctx->cache[kCacheSample]) return;
+  for (auto& kv : ctx_cache<SamplePlans>(ctx, kCacheSample))
+    for (auto& b : kv.second.mid)
+      if (b.rows) cudaFree(b.rows);
+  ctx_cache_free<SamplePlans>(ctx, kCacheSample);
 }
 
 // ---------------------------------------------------------------------------
@@ -896,21 +888,11 @@ struct HeavyPlan {
   std::vector<uint64_t> bit_off;  // word offset of giant slice i's tb (rb follows)
   uint64_t bit_words = 0;
 };
-static uint32_t heavy_big() {  // NTCB_HEAVY_BIG: log2 of the slice length above which the bitmap path runs
-  static const uint32_t w = [] {
-    const char* e = std::getenv("NTCB_HEAVY_BIG");
-    return 1u << (e ? std::max(16, std::min(30, std::atoi(e))) : 24);
-  }();
-  return w;
-}
-static uint32_t heavy_window() {  // NTCB_HEAVY_WIN: log2 of the draw window (entries)
-  static const uint32_t w = [] {
-    const char* e = std::getenv("NTCB_HEAVY_WIN");
-    return 1u << (e ? std::max(16, std::min(30, std::atoi(e))) : 24);
-  }();
-  return w;
-}
-static std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>, HeavyPlan> g_heavy;
+// slice length above which the bitmap path runs / the draw window (entries),
+// from the context's tuning (log2, validated to [16, 30] by ntcb_set_tuning)
+static uint32_t heavy_big(const ntcb_context* ctx) { return 1u << ctx->tune.heavy_big_log2; }
+static uint32_t heavy_window(const ntcb_context* ctx) { return 1u << ctx->tune.heavy_win_log2; }
+using HeavyPlans = std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t>, HeavyPlan>;
 
 int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
                         uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
@@ -919,6 +901,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   if (v.max_slice <= cap || c >= 1.0) return 0;
   uint64_t cbits;
   std::memcpy(&cbits, &c, 8);
+  auto& g_heavy = ctx_cache<HeavyPlans>(ctx, kCacheHeavy);
   auto key = std::make_tuple(static_cast<const void*>(v.off), row_begin, row_end, cbits, cap);
   auto it = g_heavy.find(key);
   if (it == g_heavy.end()) {
@@ -936,7 +919,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     // grids so fewer of their tables are in flight at once, L2 footprint),
     // then slices whose table is too long to stay in L2 alongside its
     // neighbours (windowed draws, bitmap-assisted tail and head, one per launch)
-    const uint32_t big = std::min(heavy_big(), heavy_window());
+    const uint32_t big = std::min(heavy_big(ctx), heavy_window(ctx));
     std::stable_partition(hr.begin(), hr.end(), [](const HeavyRow& h) { return h.n <= kMidSlice; });
     std::stable_partition(hr.begin(), hr.end(), [big](const HeavyRow& h) { return h.n <= big; });
     HeavyPlan pl{nullptr, static_cast<uint32_t>(hr.size()), maxn, 0, {}};
@@ -979,8 +962,8 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   // few hundred thousand entries otherwise launch ~300 mostly idle CTAs
   // each (config 4: 1000 slices of 500K entries, CTA-launch bound; kPer = 8 measured
   // best: config 4 tail phase 5.06 -> 2.40 ms per mode).
-  // NTCB_HEAVY_PER overrides kPer for experiments.
-  static const uint64_t per = [] { const char* e = std::getenv("NTCB_HEAVY_PER"); return e ? std::max(1, std::atoi(e)) : 8; }();
+  // ntcb_tuning.heavy_per overrides kPer for experiments.
+  const uint64_t per = static_cast<uint64_t>(ctx->tune.heavy_per);
   const uint64_t maxn = it->second.maxn;
   auto gx = [&](uint64_t work) {
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
@@ -1010,7 +993,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   if (hp.bit_words) NTCB_CUDA(cudaMemsetAsync(hp.bits, 0, sizeof(uint32_t) * hp.bit_words, stream));
   for (size_t i = 0; i < hp.giant.size(); ++i) {
     const HeavyRow& h = hp.giant[i];
-    const uint32_t W = heavy_window();
+    const uint32_t W = heavy_window(ctx);
     for (uint64_t w0 = 0; w0 < h.n; w0 += W) {
       const uint64_t w1 = std::min<uint64_t>(h.n, w0 + W);
       const uint64_t jend = std::min<uint64_t>(h.b, w1);
@@ -1047,18 +1030,12 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
 }
 
 void drop_heavy(ntcb_context* ctx) {
-  for (auto it = g_heavy.begin(); it != g_heavy.end();) {
-    bool mine = false;
-    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
-      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
-    if (mine) {
-      if (it->second.rows) cudaFree(it->second.rows);
-      if (it->second.bits) cudaFree(it->second.bits);
-      it = g_heavy.erase(it);
-    } else {
-      ++it;
-    }
+  if (!ctx->cache[kCacheHeavy]) return;
+  for (auto& kv : ctx_cache<HeavyPlans>(ctx, kCacheHeavy)) {
+    if (kv.second.rows) cudaFree(kv.second.rows);
+    if (kv.second.bits) cudaFree(kv.second.bits);
   }
+  ctx_cache_free<HeavyPlans>(ctx, kCacheHeavy);
 }
 
 // Host launcher.  Returns the number of kernel launches issued.

@@ -1243,8 +1243,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
   double* vv = gd + 64;
   double* P = reinterpret_cast<double*>(smem_f + W::words(a.no, R));  // [kWarps][kFinPass]
   const int NE = R * R + R;
+  __shared__ int stop;
   for (uint64_t f = blockIdx.x; f < a.n_fins; f += gridDim.x) {
-    if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
+    // one read of the error key for the whole CTA: warps that disagreed on it
+    // would leave the barriers below with stale partial sums in P[]
+    if (threadIdx.x == 0) stop = *reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull;
+    __syncthreads();
+    if (stop) return;
     const FinItem fi = a.fins[f];
     // the row's slot-group sums (k_slot_groups), contiguous group ranges per
     // warp, combined in warp order below
@@ -1292,11 +1297,35 @@ struct WorkPlan {
   uint64_t n_items = 0, n_fins = 0, n_slots = 0, n_small = 0, n_groups = 0;
   uint64_t n_entries = 0;  // entries over all items
 };
-static std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan> g_plans;
+using WorkPlans = std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, WorkPlan>;
 
+// Segment length of a mode: a function of the WHOLE mode view and the
+// device's SM count only -- never of the row range a call covers -- so every
+// row is cut into the same items, and its partial sums are associated the same
+// way, under any row partition: results are bitwise identical for 1, 2, 4 or
+// 8 GPUs (the reference's thread/schedule invariance, nmc.hpp:89-92,
+// test_nmc.cpp:337-358).  The length targets ~4 items per resident warp on
+// the thinnest shard the box runs (1/8 of the view), at least 2048 entries
+// (256 for views under 4M entries, e.g. config 1, whose 2500-entry rows were
+// latency bound on one warp) and at most kSeg.
+uint64_t segment_length(const ntcb_context* ctx, int mode) {
+  const uint64_t* off = ctx->views[mode].h_off;
+  const uint64_t total = off[ctx->views[mode].rows] - off[0];
+  constexpr uint64_t kMaxShards = 8;
+  const uint64_t target = 4ull * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps * kMaxShards;
+  const uint64_t want = (total / target + 127) / 128 * 128;
+  return std::min<uint64_t>(kSeg, std::max<uint64_t>(total < (4ull << 20) ? 256 : 2048, want));
+}
+
+// Work items of rows [r0, r1): a row of up to segment_length() entries is
+// one item, finalised in place; a longer row is cut into items of that
+// length from its start (their partial sums go to slots, summed in fp64 by
+// the finalise kernels in a fixed order).  The cut depends on the row and
+// the mode only, never on [r0, r1): any row partition gives the same bits.
 static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, double c) {
   uint64_t cbits;
   std::memcpy(&cbits, &c, 8);
+  auto& g_plans = ctx_cache<WorkPlans>(ctx, kCacheUpdate);
   auto key = std::make_tuple(static_cast<const void*>(ctx->views[mode].off), mode, r0, r1, cbits);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) return it->second;
@@ -1304,17 +1333,7 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
   std::vector<WorkItem> items;
   std::vector<FinItem> fins;
   int64_t slot = 0;
-  // Segment length: at most kSeg, and short enough that the range yields ~4
-  // items per resident warp (a row shard of a multi-GPU run has few rows).
-  static const uint64_t ipw = [] { const char* e = std::getenv("NTCB_ITEMS_PER_WARP"); return e ? std::max(1, std::atoi(e)) : 4; }();
-  const uint64_t target = ipw * static_cast<uint64_t>(ctx->sm_count) * 2 * kWarps;
-  const uint64_t total = off[r1] - off[r0];
-  // Small ranges (< 4M entries, e.g. config 1) are cut down to 256-entry
-  // segments: one warp streaming a whole 2500-entry row was latency bound
-  // (config 1: 0.212 -> 0.179 ms per AO iteration); larger ranges keep
-  // 2048-entry segments at least (measured best for 2-8-way shards).
-  const uint64_t want = (total / target + 127) / 128 * 128;
-  const uint64_t seg = std::min<uint64_t>(kSeg, std::max<uint64_t>(total < (4ull << 20) ? 256 : 2048, want));
+  const uint64_t seg = segment_length(ctx, mode);
   for (uint64_t p = r0; p < r1; ++p) {
     const uint64_t n = off[p + 1] - off[p];
     if (blocksize_for(c, n) == 0) continue;  // skipped row (nmc.cpp:237)
@@ -1365,19 +1384,37 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
 }
 
 void drop_plans(ntcb_context* ctx) {
-  for (auto it = g_plans.begin(); it != g_plans.end();) {
-    bool mine = false;
-    for (int m = 0; m < NTCB_MAX_ORDER; ++m)
-      if (std::get<0>(it->first) == static_cast<const void*>(ctx->views[m].off)) mine = true;
-    if (mine) {
-      if (it->second.d_items) cudaFree(it->second.d_items);
-      if (it->second.d_fins) cudaFree(it->second.d_fins);
-      if (it->second.d_groups) cudaFree(it->second.d_groups);
-      it = g_plans.erase(it);
-    } else {
-      ++it;
-    }
+  if (!ctx->cache[kCacheUpdate]) return;
+  for (auto& kv : ctx_cache<WorkPlans>(ctx, kCacheUpdate)) {
+    if (kv.second.d_items) cudaFree(kv.second.d_items);
+    if (kv.second.d_fins) cudaFree(kv.second.d_fins);
+    if (kv.second.d_groups) cudaFree(kv.second.d_groups);
   }
+  ctx_cache_free<WorkPlans>(ctx, kCacheUpdate);
+}
+
+// Average item length of a mode over its whole view below the tuning's
+// short_row (cached as a host-only pseudo plan, row range ~0..~0).
+static bool mode_short_rows(ntcb_context* ctx, int mode, double c) {
+  auto& g_plans = ctx_cache<WorkPlans>(ctx, kCacheUpdate);
+  uint64_t cbits;
+  std::memcpy(&cbits, &c, 8);
+  auto key = std::make_tuple(static_cast<const void*>(ctx->views[mode].off), mode, ~0ull, ~0ull, cbits);
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    WorkPlan st;
+    const uint64_t* off = ctx->views[mode].h_off;
+    const uint64_t seg = segment_length(ctx, mode);
+    for (uint64_t p = 0; p < ctx->views[mode].rows; ++p) {
+      const uint64_t n = off[p + 1] - off[p];
+      if (blocksize_for(c, n) == 0) continue;
+      st.n_items += (n + seg - 1) / seg;
+      st.n_entries += n;
+    }
+    it = g_plans.emplace(key, st).first;
+  }
+  const WorkPlan& st = it->second;
+  return st.n_items && st.n_entries < static_cast<uint64_t>(ctx->tune.short_row) * st.n_items;
 }
 
 template <int LD4, int NO>
@@ -1404,11 +1441,8 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
   const size_t warp_bytes = smem / kWarps;
   const uint64_t per_sm_items = (pl.n_items + 2 * ctx->sm_count - 1) / (2 * ctx->sm_count);
   // 4-warp CTAs (4 per SM): 3.6 % faster than 8-warp CTAs on config 2 at the
-  // same 16 warps/SM (measured); NTCB_UPDATE_WPC overrides for experiments
-  static const int wmax = [] {
-    const char* e = std::getenv("NTCB_UPDATE_WPC");
-    return e ? std::max(1, std::min(kWarps, std::atoi(e))) : 4;
-  }();
+  // same 16 warps/SM (measured); ntcb_tuning.update_wpc overrides for experiments
+  const int wmax = ctx->tune.update_wpc;
   const int wpc = static_cast<int>(std::min<uint64_t>(wmax, std::max<uint64_t>(1, per_sm_items)));
   smem = warp_bytes * wpc;
   NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1431,8 +1465,6 @@ static int launch_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_
   return launch_items_tc<P, 3>(ctx, a, pl, smem);
 }
 
-static bool g_tc_off = std::getenv("NTCB_NO_TC") != nullptr;  // A/B switch: CUDA-core Gram
-
 template <int LD4>
 static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   using W = WarpSmem<LD4>;
@@ -1441,17 +1473,18 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // feature blocks of k' = (k, x), pair layout (the 16-byte quad layout reads
   // whole 128-byte rows and measured 40% slower at rank 20)
   int P = (a.rank + 1 + 7) / 8;
-  // experiment knob: NTCB_TC_P=4 runs the quad layout (one 16-byte load per
-  // pick and mode, features 4g..4g+3) at any rank <= 31
-  static const int p_env = [] { const char* e = std::getenv("NTCB_TC_P"); return e ? std::atoi(e) : 0; }();
-  if (p_env > P && p_env <= 4) P = p_env;
+  // tuning knob tc_p = 4 runs the quad layout (one 16-byte load per pick and
+  // mode, features 4g..4g+3) at any rank <= 31
+  if (ctx->tune.tc_p > P && ctx->tune.tc_p <= 4) P = ctx->tune.tc_p;
   // ranks 32-39 (P = 5) compile but stay on the CUDA-core kernel: at one CTA
   // per SM the pair-layout gathers of three factors measured 21 ms vs 17.6 ms
   // per mode on config 4
-  static const bool nat_off = std::getenv("NTCB_NO_NAT") != nullptr;  // A/B switch
-  // rows of fewer than kShortRow entries on average: per-row latencies dominate
-  static const uint64_t short_row = [] { const char* e = std::getenv("NTCB_SHORT_ROW"); return e ? std::atoll(e) : 2048ll; }();
-  const bool short_rows = pl.n_items && pl.n_entries < short_row * pl.n_items;
+  const bool g_tc_off = ctx->tune.no_tc != 0;  // A/B switch: CUDA-core Gram
+  const bool nat_off = ctx->tune.no_nat != 0;  // A/B switch
+  // modes whose items average fewer than short_row entries over the WHOLE
+  // view (a property of the mode, not of a shard: the instantiation must not
+  // depend on the partition) -- per-row latencies dominate there
+  const bool short_rows = mode_short_rows(ctx, a.mode, a.c);
   if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && a.rank >= 25 && (a.no == 2 || a.no == 3)) {
     // ranks 25-32: natural-layout gathers through a shared tile into the
     // tensor-core Gram (w on the CUDA cores)

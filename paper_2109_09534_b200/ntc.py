@@ -196,6 +196,23 @@ class Context:
         except Exception:
             pass
 
+    # launch policy (ntcb_tuning; never changes results) ------------------
+    def tuning(self) -> dict:
+        t = _lib.TuningC()
+        check(self.L.ntcb_get_tuning(self.h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in _lib.TuningC._fields_}
+
+    def set_tuning(self, **kw) -> None:
+        """Change launch-policy knobs (A/B measurements), e.g.
+        set_tuning(no_tc=1) or set_tuning(heavy_win_log2=16)."""
+        t = _lib.TuningC()
+        check(self.L.ntcb_get_tuning(self.h, C.byref(t)))
+        for k, v in kw.items():
+            if k not in dict(_lib.TuningC._fields_):
+                raise InvalidArgument(f"tuning: unknown field {k}")
+            setattr(t, k, int(v))
+        check(self.L.ntcb_set_tuning(self.h, C.byref(t)))
+
     # tensor -------------------------------------------------------------
     def load(self, dims, indices, values):
         dims = np.ascontiguousarray(dims, np.uint64)
