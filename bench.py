@@ -139,87 +139,158 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref) on a bounded row sample of the same tensor
+# The reference on the host cores (oracle/_ref: the reference's own sources
+# compiled by oracle/Makefile).  Inputs come from the host restatement of the
+# repo's generator (oracle/synth_host.c, bit-identical to csrc/synth.cu,
+# pinned by tests/test_gpu_synth_host.py): nothing here loads libntcb.so.
 # ---------------------------------------------------------------------------
-def sample_rows(ctx, order, target_per_mode=12_000_000):
-    """Per-mode row prefix whose sampled entries reach ~target (bounded CPU sample)."""
-    from paper_2109_09534_b200.dist import blocksizes
-    out = []
-    for m in range(order):
-        cum = np.cumsum(blocksizes(ctx.view_offsets(m), 0.5).astype(np.int64))
-        out.append(int(min(len(cum), np.searchsorted(cum, target_per_mode) + 1)))
-    return out
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def reference_sample(ctx, cfgd, rows, steps, threads):
-    """Times the reference's s_nmc (RefProblem -> libntc_ref.so) on the first
-    rows[m] rows of every mode view of the tensor held by `ctx` (row prefixes
-    keep the reference's row streams identical to the full problem).  Returns
-    (sampled nnz/s, seconds of s_nmc, sampled, per-step s)."""
+def host_tensor(cfgd, cid, canonical=False):
     import oracle as O
-    dims = cfgd["dims"]
-    N, R = len(dims), cfgd["R"]
-    views = []
-    for m in range(N):
-        off, oth, val = ctx.view_rows(m, 0, rows[m])
-        views.append((off, oth, val.astype(np.float64)))
-    rp = O.RefProblem(dims, views=views)
-    F = O.ref_initial_factors(dims, R, SEED_SOLVER)
-    rp.set_factors(R, F)
-    cfg = O.nmc_cfg(lambda_=1e-3, c=0.5, max_inner=1, threads=threads)
+    return O.host_synth(cfgd["dims"], cfgd["nnz"], cfgd["true_rank"], cfgd["sigma"], 1000 + cid,
+                        cfgd.get("zipf"), cfgd.get("kind", 0), canonical=canonical)
+
+
+def ref_sweeps(rp, order, sweeps, first, threads, rows=None):
+    """AO iterations of the reference as ao_ntc runs them (ao.cpp:121-124):
+    s_nmc on every mode with sweep_stream(seed, k, i); each timed on the
+    steady clock around the s_nmc calls (the convention of ao.cpp:93 /
+    main.cpp:374).  rows: row-prefix views (the factor being updated is cut
+    to the prefix for its call, the others stay whole; untimed).  Returns
+    (seconds per sweep list, sampled entries)."""
+    import oracle as O
     orc = O.Oracle()
-    tot_s, tot_n, per = 0.0, 0, []
-    for k in range(steps):
-        t_step = 0.0
-        for m in range(N):
-            a, _ = rp.get_factor(m)
-            rp.set_factor_rows(m, a[:rows[m]])
+    cfg = O.nmc_cfg(lambda_=1e-3, c=0.5, max_inner=1, threads=threads)
+    per, n = [], 0
+    for k in range(first, first + sweeps):
+        dt = 0.0
+        for m in range(order):
+            if rows is not None:
+                a, _ = rp.get_factor(m)
+                rp.set_factor_rows(m, a[: rows[m]])
             t0 = time.perf_counter()
-            n = rp.s_nmc(m, cfg, orc.sweep_state(SEED_SOLVER, k, m))
-            dt = time.perf_counter() - t0
-            a_s, _ = rp.get_factor(m, rows[m])
-            a[:rows[m]] = a_s
-            rp.set_factor_rows(m, a)
-            t_step += dt
-            tot_n += n
-        per.append(t_step)
-        tot_s += t_step
-    return tot_n / tot_s, tot_s, tot_n, per
+            n += rp.s_nmc(m, cfg, orc.sweep_state(SEED_SOLVER, k, m))
+            dt += time.perf_counter() - t0
+            if rows is not None:
+                a_s, _ = rp.get_factor(m, rows[m])
+                a[: rows[m]] = a_s
+                rp.set_factor_rows(m, a)
+        per.append(dt)
+    return per, n
 
 
-def full_sampled_per_sweep(ctx, order):
-    from paper_2109_09534_b200.dist import blocksizes
-    return int(sum(int(blocksizes(ctx.view_offsets(m), 0.5).sum()) for m in range(order)))
+def reference_problem(cfgd, cid, R):
+    """The reference's own SparseTensor (validation + lexicographic sort,
+    sparse_tensor.cpp:24-73) and build_mode_views (mode_view.cpp:8-37) on the
+    host-generated tensor (generation order, as a loader would hand it over),
+    and initial_factors(dims, R, 7) (ao.cpp:70-73)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    idx, vals = host_tensor(cfgd, cid)
+    t1 = time.perf_counter()
+    rp = O.RefProblem(cfgd["dims"], idx, vals.astype(np.float64))
+    t2 = time.perf_counter()
+    del idx, vals
+    rp.set_factors(R, O.ref_initial_factors(cfgd["dims"], R, SEED_SOLVER))
+    return rp, {"generate_s": t1 - t0, "sparse_tensor_and_views_s": t2 - t1}
+
+
+def speedup_curve():
+    """The paper-style thread scaling point (main.cpp:394-400): config 1 with
+    1 thread and with every host thread, full AO iterations."""
+    c1 = CONFIGS[1]
+    rp, _ = reference_problem(c1, 1, c1["R"])
+    allt = os.cpu_count() or 1
+    out = {}
+    for th in (1, allt):
+        ref_sweeps(rp, 3, 1, 0, th)  # warm-up sweep
+        per, _ = ref_sweeps(rp, 3, 3, 1, th)
+        out[str(th)] = statistics.median(per)
+    return {"config": "cfg1 (500^3, 1.25M, R 10, c 0.5)", "sec_per_ao_iteration_by_threads": out,
+            "speedup": out["1"] / out[str(allt)]}
 
 
 def run_reference(args, cfgd, cid):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2109_09534_b200 as P
-    ctx = P.Context(0)  # data generation only (device generator, bit-identical inputs)
-    generate(ctx, cfgd, cid)
-    order = len(cfgd["dims"])
-    full = full_sampled_per_sweep(ctx, order)
+    dims, R = cfgd["dims"], cfgd["R"]
+    order = len(dims)
     threads = os.cpu_count() or 1
-    S = sample_rows(ctx, order)
-    rate_w, _, _, _ = reference_sample(ctx, cfgd, S, args.warmup, threads) if args.warmup else (0, 0, 0, [])
-    rate, secs, n, per = reference_sample(ctx, cfgd, S, args.steps, threads)
-    sample = (f"first {S} rows of the {order} mode views per step "
-              f"({n // max(args.steps, 1)} sampled entries/step); s_nmc wall time only "
-              f"(steady_clock convention of ao.cpp:93)")
+    rp, setup = reference_problem(cfgd, cid, R)
+    if args.warmup:
+        ref_sweeps(rp, order, args.warmup, 0, threads)
+    per, n = ref_sweeps(rp, order, args.steps, args.warmup, threads)
+    secs = sum(per)
+    rate = n / secs
+    curve = speedup_curve() if cid != 1 else None
     out = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * secs / max(args.steps, 1), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device generator, seeded)",
-        "config": {"workload": workload_name(cid, cfgd), "sample_rows_per_mode": S},
-        "sec_per_ao_iteration": full / rate,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (oracle/synth_host.c: the repo's seeded generator restated on the host, "
+                "bit-identical)",
+        "config": {"workload": workload_name(cid, cfgd), "dims": dims, "nnz": cfgd["nnz"], "rank": R,
+                   "c": 0.5, "max_inner": 1, "lambda": 1e-3, "same_config": True,
+                   "sampled_per_ao_iteration": n // max(args.steps, 1)},
+        "sec_per_ao_iteration": secs / max(args.steps, 1),
+        "sec_per_ao_iteration_median": statistics.median(per),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} full AO iterations (s_nmc over every mode, sweep_stream "
+                                   f"replay of ao.cpp:121-124) after {args.warmup} warm-up iterations, "
+                                   f"{threads} OpenMP threads; the reference's own SparseTensor + "
+                                   f"build_mode_views, built before the timer"},
+        "setup": setup,
+        "thread_scaling": curve,
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_sample(cfgd, cid):
+    """cpu_baseline of our arm: the reference's s_nmc (oracle/_ref) on row
+    prefixes of every mode view, ~10 s of host work.  The views are built on
+    the host (oracle/synth_host.c canonical COO -> the C restatement's
+    build_view, mode_view.cpp:8-37); row prefixes keep the reference's row
+    streams identical to the full problem."""
+    import oracle as O
+    from paper_2109_09534_b200.dist import blocksizes
+    dims, R = cfgd["dims"], cfgd["R"]
+    order = len(dims)
+    threads = os.cpu_count() or 1
+    idx, vals = host_tensor(cfgd, cid, canonical=True)
+    orc = O.Oracle()
+    views, rows = [], []
+    for m in range(order):
+        off, oth, val = orc.build_view(dims, idx, vals.astype(np.float64), m)
+        cum = np.cumsum(blocksizes(off, 0.5).astype(np.int64))
+        r = int(min(len(cum), np.searchsorted(cum, 12_000_000) + 1))
+        e1 = int(off[r])
+        views.append((off[: r + 1].copy(), oth[:e1].copy(), val[:e1].copy()))
+        rows.append(r)
+        del off, oth, val
+    del idx, vals
+    rp = O.RefProblem(dims, views=views)
+    rp.set_factors(R, O.ref_initial_factors(dims, R, SEED_SOLVER))
+    per1, _ = ref_sweeps(rp, order, 1, 0, threads, rows)
+    sweeps = int(min(40, max(2, round(10.0 / max(per1[0], 1e-3)))))
+    per, n = ref_sweeps(rp, order, sweeps, 1, threads, rows)
+    return {"value": n / sum(per), "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"oracle/_ref s_nmc on the first {rows} rows of the mode views (built on the host), "
+                      f"{sweeps} sweeps, {n} sampled entries in {sum(per):.1f} s"}
 
 
 # ---------------------------------------------------------------------------
@@ -401,18 +472,7 @@ def run_ours(args, cfgd, cid):
                        f"full factor device -> pinned host (rank-local bytes)"}
 
     # ---- CPU baseline: the reference on this box's cores (rank 0, N=1) -----------
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        import oracle  # noqa: F401  (checker/baseline only)
-        threads = os.cpu_count() or 1
-        S = sample_rows(ctx, order)
-        # a bounded sample of ~10 s of CPU work: sweeps over the row prefixes
-        _, s1, _, _ = reference_sample(ctx, cfgd, S, 1, threads)
-        sweeps = int(min(40, max(2, round(10.0 / max(s1, 1e-3)))))
-        rate, secs, n, _ = reference_sample(ctx, cfgd, S, sweeps, threads)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-               "sample": f"oracle/_ref s_nmc on the first {S} rows of the mode views, {sweeps} sweeps, "
-                         f"{n} sampled entries in {secs:.1f} s"}
+    cpu = cpu_baseline_sample(cfgd, cid) if (world == 1 and not args.no_cpu) else None
 
     if rank == 0:
         out = {

@@ -111,6 +111,8 @@ class Oracle:
         L.orc_relative_error.argtypes = [C.c_int, _u64p, C.c_uint64, C.POINTER(_f64p), C.c_uint64,
                                          _u32p, _f64p, _f64p]
         L.orc_initial_factors.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, _f64p]
+        L.ntco_synth.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, _f64p,
+                                 C.c_int, C.c_int, C.c_int, _u32p, C.POINTER(C.c_float)]
 
     def _check(self, rc):
         if rc:
@@ -234,6 +236,27 @@ class Oracle:
 # The reference itself (oracle/_ref/libntc_ref.so)
 # --------------------------------------------------------------------------
 _REF = None
+
+
+def host_synth(dims, nnz, true_rank, sigma, seed, zipf_alpha=None, value_kind=0, canonical=False,
+               threads=None):
+    """The repo's synthetic tensor generated on the host cores
+    (oracle/synth_host.c, a C restatement of csrc/synth.cu, bit-identical):
+    (indices (nnz, N) uint32, values float32), in generation order (what the
+    device canonicalises) or, with canonical=True, lexicographic order."""
+    L = Oracle().L
+    N = len(dims)
+    d = np.ascontiguousarray(dims, np.uint64)
+    z = None if zipf_alpha is None else np.ascontiguousarray(zipf_alpha, np.float64)
+    idx = np.empty(max(nnz * N, 1), np.uint32)
+    vals = np.empty(max(nnz, 1), np.float32)
+    rc = L.ntco_synth(N, _ptr(d, _u64p), nnz, true_rank, sigma, seed, _ptr(z, _f64p), value_kind,
+                      1 if canonical else 0, threads or os.cpu_count() or 1,
+                      _ptr(idx, _u32p), vals.ctypes.data_as(C.POINTER(C.c_float)))
+    if rc:
+        raise ValueError({1: "host_synth: invalid configuration", 2: "host_synth: too many candidates",
+                          3: "host_synth: out of memory"}.get(rc, f"host_synth: error {rc}"))
+    return idx[: nnz * N].reshape(nnz, N), vals[:nnz]
 
 
 def ref_available() -> bool:

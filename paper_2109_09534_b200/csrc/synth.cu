@@ -16,8 +16,12 @@
 //   kind 0: sum_r prod_m U_m[i_m, r] + sigma g_j, clamped at 0;
 //   kind 1: round(clip(1 + 4 * (sum_r prod_m U_m[i_m, r]) / R_true + sigma g_j, 1, 5))
 //           (the 1-5 rating model of BASELINE configs[2]);
-// g_j is the reference's Box-Muller (rng.hpp:49-53) on fork(fork(seed, 6), j).
-// Tags 4..6 follow synth.cpp:16-18.
+// g_j is the reference's Box-Muller (rng.hpp:49-53) on fork(fork(seed, 6), j),
+// with log and cos evaluated by fixed series (det_log, det_cos2pi) and every
+// floating-point operation an explicitly rounded + - * / sqrt (no FMA
+// contraction): the values are reproducible bit for bit on the host, which
+// the reference arm of bench.py relies on (oracle/synth_host.c, pinned by
+// tests/test_gpu_synth_host.py).  Tags 4..6 follow synth.cpp:16-18.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -104,6 +108,45 @@ __global__ void k_truth(uint64_t root, uint64_t n, double* out) {
     out[q] = static_cast<double>(mix64(root + (q + 1) * kGolden) >> 11) * 0x1.0p-53;
 }
 
+// log(x), x in (0, 1]: x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// log m = 2 s (1 + z/3 + ... + z^11/23), s = (m - 1)/(m + 1), z = s^2
+__device__ double det_log(double x) {
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+  int e = static_cast<int>((b >> 52) & 0x7ff) - 1023;
+  b = (b & 0xfffffffffffffull) | (1023ull << 52);
+  double m = __longlong_as_double(static_cast<long long>(b));
+  if (m > 1.4142135623730951) {
+    m = __dmul_rn(m, 0.5);
+    e += 1;
+  }
+  const double s = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0));
+  const double z = __dmul_rn(s, s);
+  double p = __ddiv_rn(1.0, 23.0);
+  for (int k = 10; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, z), __ddiv_rn(1.0, static_cast<double>(2 * k + 1)));
+  return __dadd_rn(__dmul_rn(static_cast<double>(e), 0.6931471805599453), __dmul_rn(__dmul_rn(2.0, s), p));
+}
+
+// cos(2 pi u), u in [0, 1): quadrant q = floor(4u), a = (4u - q) pi/2,
+// Taylor series of cos a and sin a to the a^22 / a^23 term (Horner)
+__device__ double det_cos2pi(double u) {
+  const double t = __dmul_rn(4.0, u);
+  const int q = static_cast<int>(t);
+  const double a = __dmul_rn(__dsub_rn(t, static_cast<double>(q)), 1.5707963267948966);
+  const double z = __dmul_rn(a, a);
+  double c = 1.0, sn = 1.0;
+  for (int k = 11; k >= 1; --k) {
+    c = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(z, static_cast<double>((2 * k - 1) * (2 * k))), c));
+    sn = __dsub_rn(1.0, __dmul_rn(__ddiv_rn(z, static_cast<double>((2 * k) * (2 * k + 1))), sn));
+  }
+  sn = __dmul_rn(a, sn);
+  switch (q & 3) {
+    case 0: return c;
+    case 1: return -sn;
+    case 2: return -c;
+    default: return sn;
+  }
+}
+
 __global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d, int R,
                        const double* const* truth, uint64_t noise_root, double sigma, int kind,
                        uint32_t* idx, float* vals) {
@@ -118,8 +161,8 @@ __global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d
     double model = 0.0;
     for (int r = 0; r < R; ++r) {
       double prod = 1.0;
-      for (int m = 0; m < d.order; ++m) prod *= truth[m][static_cast<uint64_t>(ix[m]) * R + r];
-      model += prod;
+      for (int m = 0; m < d.order; ++m) prod = __dmul_rn(prod, truth[m][static_cast<uint64_t>(ix[m]) * R + r]);
+      model = __dadd_rn(model, prod);
     }
     double g = 0.0;
     if (sigma > 0.0) {
@@ -128,14 +171,14 @@ __global__ void k_emit(const uint32_t* js, uint64_t nnz, uint64_t s_mask, Dims d
       const double u1 = static_cast<double>((mix64(s) >> 11) + 1) * 0x1.0p-53;
       s += kGolden;
       const double u2 = static_cast<double>(mix64(s) >> 11) * 0x1.0p-53;
-      g = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+      g = __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, det_log(u1))), det_cos2pi(u2));
     }
     double v;
     if (kind == 1) {
-      v = 1.0 + 4.0 * model / R + sigma * g;
+      v = __dadd_rn(__dadd_rn(1.0, __ddiv_rn(__dmul_rn(4.0, model), static_cast<double>(R))), __dmul_rn(sigma, g));
       v = rint(fmin(fmax(v, 1.0), 5.0));
     } else {
-      v = model + sigma * g;
+      v = __dadd_rn(model, __dmul_rn(sigma, g));
       v = v > 0.0 ? v : 0.0;
     }
     vals[e] = static_cast<float>(v);
