@@ -111,6 +111,8 @@ class Oracle:
         L.orc_relative_error.argtypes = [C.c_int, _u64p, C.c_uint64, C.POINTER(_f64p), C.c_uint64,
                                          _u32p, _f64p, _f64p]
         L.orc_initial_factors.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, _f64p]
+        L.orc_sample_mask_rows.argtypes = [C.c_uint64, _u64p, C.c_double, C.c_uint64,
+                                           C.POINTER(C.c_uint8), C.c_int]
         L.ntco_synth.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, _f64p,
                                  C.c_int, C.c_int, C.c_int, _u32p, C.POINTER(C.c_float)]
 
@@ -143,6 +145,15 @@ class Oracle:
         picks = np.zeros(max(n, 1), np.uint32)
         b = self.L.orc_sample_row(n, c, state, _ptr(picks, _u32p))
         return picks[:b].copy()
+
+    def sample_mask_rows(self, off, c, root, threads=None):
+        """Per-entry 0/1 array of the sampled sets of every row of a view
+        (row streams fork(root, p)), computed on the host cores."""
+        off = np.ascontiguousarray(off, np.uint64)
+        out = np.zeros(max(int(off[-1]), 1), np.uint8)
+        self.L.orc_sample_mask_rows(len(off) - 1, _ptr(off, _u64p), c, root,
+                                    out.ctypes.data_as(C.POINTER(C.c_uint8)), threads or os.cpu_count() or 1)
+        return out[: int(off[-1])]
 
     # tensor / views
     def canonicalize(self, dims, idx, vals):

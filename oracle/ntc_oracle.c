@@ -116,6 +116,34 @@ uint64_t orc_sample_row(uint64_t n, double c, uint64_t state, uint32_t* picks) {
   return b;
 }
 
+/* Sampled set of every row of a view, sample_row with the row stream
+ * fork(root, p) (nmc.cpp:236): out[e] = 1 for the picked entries of each
+ * slice (absolute view positions, rows in parallel). */
+void orc_sample_mask_rows(uint64_t rows, const uint64_t* off, double c, uint64_t root, uint8_t* out,
+                          int threads) {
+#pragma omp parallel num_threads(threads)
+  {
+    uint64_t cap = 0;
+    uint32_t *picks = NULL, *perm = NULL;
+#pragma omp for schedule(dynamic, 16)
+    for (uint64_t p = 0; p < rows; ++p) {
+      const uint64_t n = off[p + 1] - off[p];
+      if (n > cap) {
+        free(picks);
+        free(perm);
+        cap = n;
+        picks = (uint32_t*)malloc(sizeof(uint32_t) * cap);
+        perm = (uint32_t*)malloc(sizeof(uint32_t) * cap);
+      }
+      memset(out + off[p], 0, n);
+      const uint64_t b = sample_into(n, c, orc_fork(root, p), picks, perm);
+      for (uint64_t j = 0; j < b; ++j) out[off[p] + picks[j]] = 1;
+    }
+    free(picks);
+    free(perm);
+  }
+}
+
 /* ---- SparseTensor canonicalisation: sparse_tensor.cpp:24-73 -------------- */
 typedef struct {
   const uint32_t* idx;
