@@ -303,6 +303,9 @@ def run_ours(args, cfgd, cid):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local} but {torch.cuda.device_count()} are visible "
+                         f"(one process per GPU)")
     torch.cuda.set_device(local)
     stream = torch.cuda.Stream()  # a real stream handle (the legacy default is NULL)
     torch.cuda.set_stream(stream)
@@ -482,6 +485,8 @@ def run_ours(args, cfgd, cid):
             "data": "synthetic (seeded device generator; BASELINE configs shape)",
             "config": {"workload": workload_name(cid, cfgd), "dims": dims, "nnz": cfgd["nnz"],
                        "exchange": (sharded.exchange if sharded else "none"),
+                       "view_bytes_this_rank": (sum(sharded.view_bytes) if sharded else
+                                                sum(ctx.view_resident(m)[2] for m in range(order))),
                        "rank": R, "c": 0.5, "max_inner": 1, "lambda": 1e-3,
                        "sampled_per_ao_iteration": full,
                        "l2": l2_note(cfgd),
@@ -516,6 +521,16 @@ def main():
     ap.add_argument("--tune", nargs="*", default=[], metavar="K=V",
                     help="ntcb_tuning launch-policy knobs for A/B runs, e.g. --tune split_rows=1")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfgd, args.config)

@@ -146,6 +146,17 @@ int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* o
  * (absolute entry positions), others/values of those slices only. */
 int ntcb_view_export_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
                           uint64_t* offsets, uint32_t* others, float* values);
+/* Slab storage for row-sharded multi-GPU runs: keep only the entries of
+ * rows [row_begin, row_end) of view `mode` on the device (within the rows
+ * already kept), freeing the rest -- every rank of an N-way run then holds
+ * ~1/N of each view.  Afterwards only calls on those rows are accepted
+ * (ntcb_s_nmc_rows_async, ntcb_sample_rows / _row / _mask, the row export);
+ * whole-mode calls fail with NTCB_ERANGE, and ntcb_metrics returns the
+ * partial sums over the kept rows of mode 0 (sum them over the ranks).
+ * ntcb_view_resident reports the kept rows and the device bytes of the view. */
+int ntcb_view_keep_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end);
+int ntcb_view_resident(ntcb_context* ctx, int mode, uint64_t* row_begin, uint64_t* row_end,
+                       uint64_t* device_bytes);
 /* Canonical (lexicographic) COO, SparseTensor::indices()/values(). */
 int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values);
 
@@ -249,7 +260,8 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
                 void* user);
 
 /* ---- metrics (metrics.cpp:8-37) ---------------------------------------- */
-/* sse = sum_Omega (x - model)^2, sumsq = sum x^2, reg = sum_m ||U_m||_F^2. */
+/* sse = sum_Omega (x - model)^2, sumsq = sum x^2, reg = sum_m ||U_m||_F^2
+ * (sse and sumsq over the kept rows of mode 0 when the view is a slab). */
 int ntcb_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg);
 int ntcb_objective(ntcb_context* ctx, double lambda, double* out);
 int ntcb_relative_error(ntcb_context* ctx, double* out);

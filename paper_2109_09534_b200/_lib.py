@@ -95,6 +95,8 @@ SIGNATURES = {
     "ntcb_view_export_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, u64p, u32p,
                                         f32p]),
     "ntcb_tensor_export": (C.c_int, [C.c_void_p, u32p, f32p]),
+    "ntcb_view_keep_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
+    "ntcb_view_resident": (C.c_int, [C.c_void_p, C.c_int, u64p, u64p, u64p]),
     "ntcb_tns_parse": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), u64p, u64p, C.POINTER(u32p),
                                  C.POINTER(f64p)]),
     "ntcb_tns_last_error": (C.c_char_p, []),

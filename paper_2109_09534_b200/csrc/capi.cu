@@ -34,6 +34,7 @@ void free_views(ntcb_context* ctx);
 void drop_plans(ntcb_context* ctx);
 void drop_heavy(ntcb_context* ctx);
 void drop_sample_plans(ntcb_context* ctx);
+void drop_metric_plans(ntcb_context* ctx);
 void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                      const uint32_t* h_idx, const double* h_vals);
 void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
@@ -83,6 +84,23 @@ void need_ctx(ntcb_context* ctx) {
 void need_tensor(ntcb_context* ctx) {
   if (ctx->order < 2) fail(NTCB_EINVAL, "ntcb: no tensor loaded");
 }
+// rows [r0, r1) of view `mode` must be resident (ntcb_view_keep_rows)
+void need_rows(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1) {
+  const DeviceView& v = ctx->views[mode];
+  if (r1 > r0 && (r0 < v.row_lo || r1 > v.row_hi))
+    fail(NTCB_ERANGE, "ntcb: rows [" + std::to_string(r0) + ", " + std::to_string(r1) + ") of mode " +
+                          std::to_string(mode + 1) + " are not resident (slab [" + std::to_string(v.row_lo) +
+                          ", " + std::to_string(v.row_hi) + "))");
+}
+bool is_slab(const ntcb_context* ctx) {
+  for (int m = 0; m < ctx->order; ++m)
+    if (ctx->views[m].row_lo != 0 || ctx->views[m].row_hi != ctx->views[m].rows) return true;
+  return false;
+}
+void need_whole(ntcb_context* ctx) {
+  for (int m = 0; m < ctx->order; ++m) need_rows(ctx, m, 0, ctx->dims[m]);
+}
+
 void need_factors(ntcb_context* ctx) {
   need_tensor(ctx);
   if (ctx->rank == 0 || !ctx->A[0]) fail(NTCB_EINVAL, "ntcb: no factors loaded");
@@ -655,6 +673,7 @@ int ntcb_view_export(ntcb_context* ctx, int mode, uint64_t* offsets, uint32_t* o
   need_ctx(ctx);
   need_tensor(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_export: mode out of range");
+  if (others || values) need_rows(ctx, mode, 0, ctx->dims[mode]);
   const DeviceView& v = ctx->views[mode];
   const uint64_t nnz = ctx->nnz;
   const int no = ctx->order - 1;
@@ -679,6 +698,7 @@ int ntcb_view_export_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint6
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_export: mode out of range");
   const DeviceView& v = ctx->views[mode];
   if (row_begin > row_end || row_end > v.rows) fail(NTCB_ERANGE, "view_export: rows out of range");
+  if (others || values) need_rows(ctx, mode, row_begin, row_end);
   const uint64_t e0 = v.h_off[row_begin], e1 = v.h_off[row_end], n = e1 - e0;
   const int no = ctx->order - 1;
   if (offsets) std::memcpy(offsets, v.h_off + row_begin, sizeof(uint64_t) * (row_end - row_begin + 1));
@@ -697,6 +717,7 @@ int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values) {
   API_TRY
   need_ctx(ctx);
   need_tensor(ctx);
+  need_rows(ctx, 0, 0, ctx->dims[0]);
   // the mode-0 view IS the canonical lexicographic order (mode_view.cpp:5-7)
   const DeviceView& v = ctx->views[0];
   const uint64_t nnz = ctx->nnz;
@@ -712,6 +733,91 @@ int ntcb_tensor_export(ntcb_context* ctx, uint32_t* indices, float* values) {
   }
   if (values && nnz)
     NTCB_CUDA(cudaMemcpy(values, v.val, sizeof(float) * nnz, cudaMemcpyDeviceToHost));
+  API_CATCH
+}
+
+int ntcb_view_keep_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_keep_rows: mode out of range");
+  if (row_begin > row_end || row_end > ctx->dims[mode]) fail(NTCB_ERANGE, "view_keep_rows: rows out of range");
+  need_rows(ctx, mode, row_begin, row_end);
+  collect(ctx, nullptr);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->side));
+  DeviceView& v = ctx->views[mode];
+  const int no = ctx->order - 1;
+  const uint64_t e0 = v.h_off[row_begin], e1 = v.h_off[row_end];
+  const uint64_t a_lo = e0 & ~uint64_t(31);  // whole 128-byte batches stay in bounds
+  const uint64_t n = e1 - a_lo + kViewPad;
+  for (int k = 0; k < no; ++k) {
+    uint32_t* nb = nullptr;
+    NTCB_CUDA(cudaMalloc(&nb, sizeof(uint32_t) * n));
+    NTCB_CUDA(cudaMemcpy(nb, v.oth[k] + a_lo, sizeof(uint32_t) * (e1 - a_lo), cudaMemcpyDeviceToDevice));
+    NTCB_CUDA(cudaMemset(nb + (e1 - a_lo), 0, sizeof(uint32_t) * kViewPad));
+    NTCB_CUDA(cudaFree(v.oth[k] + v.a_lo));
+    v.oth[k] = nb - a_lo;
+  }
+  {
+    float* nb = nullptr;
+    NTCB_CUDA(cudaMalloc(&nb, sizeof(float) * n));
+    NTCB_CUDA(cudaMemcpy(nb, v.val + a_lo, sizeof(float) * (e1 - a_lo), cudaMemcpyDeviceToDevice));
+    NTCB_CUDA(cudaMemset(nb + (e1 - a_lo), 0, sizeof(float) * kViewPad));
+    NTCB_CUDA(cudaFree(v.val + v.a_lo));
+    v.val = nb - a_lo;
+  }
+  const uint64_t words = (e1 - a_lo) / 32 + 2 + kViewPad / 32;
+  for (int q = 0; q < 2; ++q) {
+    uint32_t* nb = nullptr;
+    NTCB_CUDA(cudaMalloc(&nb, sizeof(uint32_t) * words));
+    NTCB_CUDA(cudaMemset(nb, 0, sizeof(uint32_t) * words));
+    NTCB_CUDA(cudaFree(ctx->mask[mode][q] + (v.a_lo >> 5)));
+    ctx->mask[mode][q] = nb - (a_lo >> 5);
+    ctx->consumed_valid[mode][q] = false;
+  }
+  v.a_lo = a_lo;
+  v.row_lo = row_begin;
+  v.row_hi = row_end;
+  uint64_t mx = 0;
+  for (uint64_t p = row_begin; p < row_end; ++p) mx = std::max(mx, v.h_off[p + 1] - v.h_off[p]);
+  v.max_slice = mx;
+  // the per-entry sampler scratch covers the largest resident slab
+  if (ctx->perm_scratch) {
+    uint64_t need = 0;
+    for (int m = 0; m < ctx->order; ++m) {
+      const DeviceView& w = ctx->views[m];
+      need = std::max(need, w.h_off[w.row_hi] - w.a_lo + kViewPad);
+    }
+    if (need < ctx->perm_scratch_n) {
+      uint32_t* ns = nullptr;
+      NTCB_CUDA(cudaMalloc(&ns, sizeof(uint32_t) * need));
+      NTCB_CUDA(cudaFree(ctx->perm_scratch));
+      ctx->perm_scratch = ns;
+      ctx->perm_scratch_n = need;
+    }
+  }
+  drop_plans(ctx);
+  drop_heavy(ctx);
+  drop_sample_plans(ctx);
+  drop_metric_plans(ctx);
+  host_of(ctx).bs_cache.clear();
+  API_CATCH
+}
+
+int ntcb_view_resident(ntcb_context* ctx, int mode, uint64_t* row_begin, uint64_t* row_end,
+                       uint64_t* device_bytes) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "view_resident: mode out of range");
+  const DeviceView& v = ctx->views[mode];
+  if (row_begin) *row_begin = v.row_lo;
+  if (row_end) *row_end = v.row_hi;
+  if (device_bytes) {
+    const uint64_t n = v.h_off[v.row_hi] - v.a_lo + kViewPad;
+    *device_bytes = n * 4 * static_cast<uint64_t>(ctx->order) + sizeof(uint64_t) * (v.rows + 1) +
+                    2 * sizeof(uint32_t) * (n / 32 + 2);
+  }
   API_CATCH
 }
 
@@ -828,6 +934,7 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
   validate_nmc(cfg);
   need_factors(ctx);
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  need_rows(ctx, mode, 0, ctx->dims[mode]);
   auto& hs = host_of(ctx);
   if (!a_init && !hs.verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   if (hs.queued) collect(ctx, nullptr);  // drain (and report) anything queued before
@@ -871,6 +978,7 @@ int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint6
   if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
   if (row_begin > row_end || row_end > ctx->dims[mode])
     fail(NTCB_ERANGE, "s_nmc: row range out of bounds");
+  need_rows(ctx, mode, row_begin, row_end);
   if (!host_of(ctx).verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   enqueue_snmc(ctx, mode, row_begin, row_end, *cfg, rng_state);
   API_CATCH
@@ -893,6 +1001,7 @@ int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
   if (row_begin > row_end || row_end > ctx->dims[mode])
     fail(NTCB_ERANGE, "sample_row: row out of range");
   if (!(c > 0.0 && c <= 1.0)) fail(NTCB_EINVAL, "sample_row: c must be in (0, 1]");
+  need_rows(ctx, mode, row_begin, row_end);
   const uint64_t* off = ctx->views[mode].h_off;
   const uint64_t rows = row_end - row_begin;
   std::vector<uint64_t> po(rows + 1, 0);
@@ -928,6 +1037,7 @@ int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_
   if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "sample_row: mode out of range");
   if (row >= ctx->dims[mode]) fail(NTCB_ERANGE, "sample_row: row out of range");
   if (!(c > 0.0 && c <= 1.0)) fail(NTCB_EINVAL, "sample_row: c must be in (0, 1]");
+  need_rows(ctx, mode, row, row + 1);
   const uint64_t* off = ctx->views[mode].h_off;
   const uint64_t b = blocksize_for(c, off[row + 1] - off[row]);
   if (count) *count = b;
@@ -960,6 +1070,7 @@ int ntcb_sample_mask(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
   if (row_begin > row_end || row_end > ctx->dims[mode])
     fail(NTCB_ERANGE, "sample_mask: rows out of range");
   if (!(c > 0.0 && c < 1.0)) fail(NTCB_EINVAL, "sample_mask: c must be in (0, 1)");
+  need_rows(ctx, mode, row_begin, row_end);
   collect(ctx, nullptr);
   const uint64_t* off = ctx->views[mode].h_off;
   const uint64_t e0 = off[row_begin], e1 = off[row_end];
@@ -981,6 +1092,7 @@ int ntcb_sweep_async(ntcb_context* ctx, uint64_t sweep, const ntcb_nmc_config* c
   need_ctx(ctx);
   validate_nmc(cfg);
   need_factors(ctx);
+  need_whole(ctx);
   for (int i = 0; i < ctx->order; ++i) {
     if (!host_of(ctx).verified[i]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
     enqueue_snmc(ctx, i, 0, ctx->dims[i], *cfg, ntcb_sweep_stream_state(seed, sweep, i));
@@ -1006,6 +1118,7 @@ int ntcb_objective(ntcb_context* ctx, double lambda, double* out) {
   need_ctx(ctx);
   need_factors(ctx);
   if (lambda < 0.0) fail(NTCB_EINVAL, "objective: lambda must be >= 0");
+  need_whole(ctx);
   double sse, sx, reg;
   device_metrics(ctx, &sse, &sx, &reg);
   *out = 0.5 * sse + 0.5 * lambda * reg;  // metrics.cpp:8-21
@@ -1016,6 +1129,7 @@ int ntcb_relative_error(ntcb_context* ctx, double* out) {
   API_TRY
   need_ctx(ctx);
   need_factors(ctx);
+  need_whole(ctx);
   double sse, sx, reg;
   device_metrics(ctx, &sse, &sx, &reg);
   if (sx == 0.0) fail(NTCB_EDOMAIN, "relative_error: all observed values are zero");
@@ -1028,6 +1142,7 @@ int ntcb_rmse(ntcb_context* ctx, double* out) {
   need_ctx(ctx);
   need_factors(ctx);
   if (ctx->nnz == 0) fail(NTCB_EDOMAIN, "rmse: empty observation set");
+  need_whole(ctx);
   double sse, sx, reg;
   device_metrics(ctx, &sse, &sx, &reg);
   *out = std::sqrt(sse / static_cast<double>(ctx->nnz));
@@ -1048,6 +1163,7 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
                     cfg->threads, cfg->chunk};
   validate_nmc(&n);
   need_factors(ctx);
+  need_whole(ctx);
   if (ctx->rank != cfg->rank) fail(NTCB_EINVAL, "ao_ntc: init rank differs from configured rank");
   auto& hs = host_of(ctx);
   for (int m = 0; m < ctx->order; ++m)

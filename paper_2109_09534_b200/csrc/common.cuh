@@ -67,11 +67,16 @@ constexpr uint64_t kViewPad = 160;
 
 struct DeviceView {
   uint64_t rows = 0;
-  uint64_t max_slice = 0;
+  uint64_t max_slice = 0;     // longest resident slice
   uint64_t* off = nullptr;
+  // oth/val are indexed by ABSOLUTE view position e; when the context keeps
+  // only a slab of rows (ntcb_view_keep_rows, multi-GPU shards) they point
+  // a_lo elements before their allocation, which covers [a_lo, e_hi + pad)
   uint32_t* oth[NTCB_MAX_ORDER - 1] = {};
   float* val = nullptr;
   uint64_t* h_off = nullptr;  // host copy of the offsets (shard planning, blocksizes)
+  uint64_t row_lo = 0, row_hi = 0;  // resident rows [row_lo, row_hi)
+  uint64_t a_lo = 0;                // first allocated entry (row_lo's start rounded down to 32)
 };
 
 // Kernel-argument bundle describing the factor matrices.
@@ -166,6 +171,10 @@ struct ntcb_context {
 };
 
 namespace ntcb {
+// The per-entry sampler scratch, indexed by absolute view position of `mode`.
+inline uint32_t* view_scratch(ntcb_context* ctx, int mode) {
+  return ctx->perm_scratch ? ctx->perm_scratch - ctx->views[mode].a_lo : nullptr;
+}
 // The map of cache slot k of a context, created on first use.
 template <class M>
 M& ctx_cache(ntcb_context* ctx, int k) {

@@ -199,7 +199,7 @@ const MPlan& mplan(ntcb_context* ctx) {
   const uint64_t slots = static_cast<uint64_t>(ctx->sm_count) * 32;
   const uint64_t len = std::min<uint64_t>(kItem, std::max<uint64_t>(256, (nnz / (2 * slots) + 31) / 32 * 32));
   std::vector<MItem> items;
-  for (uint64_t p = 0; p < v.rows; ++p)
+  for (uint64_t p = v.row_lo; p < v.row_hi; ++p)  // resident rows (a slab on a multi-GPU shard)
     for (uint64_t e = v.h_off[p]; e < v.h_off[p + 1]; e += len)
       items.push_back({p, e, std::min<uint64_t>(v.h_off[p + 1], e + len)});
   MPlan pl;

@@ -704,27 +704,95 @@ __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags
 // is unique to it), so each root has one writer.
 constexpr int kTailIlp = 4;
 
-// Slices whose scratch exceeds L2 (config 5: up to 261M entries): the draw
-// phase in target windows [w0, w1) of kWin entries, one slice and one window
-// per launch, so the atomics stay in L2.  Every draw j < min(b, w1) is
-// recomputed per window (only those can land there, r_j >= j) -- cheap
-// integer work instead of random DRAM read-modify-writes.
-__global__ void k_heavy_draw_win(const HeavyRow* rows, uint32_t* scratch, int* flags, uint64_t root,
-                                 int direct, uint32_t w0, uint32_t w1, uint32_t* tb) {
+// Giant slices, bucketed draw phase: the draws are sorted by target window
+// (kernel boundaries between the passes), so every draw is computed twice --
+// once to count, once to scatter -- instead of once per window it could
+// reach (r_j >= j: window k needs every j < w1, 12x the draws for a
+// 261M-entry slice), and each window's bucket is then applied with
+// L2-resident atomics.  Pass 1: per-CTA histograms over a fixed j range.
+constexpr int kGiantCtas = 1184;  // 8 x 148: CTAs of the count / scatter passes
+__device__ __forceinline__ uint32_t giant_draw(uint64_t state, uint32_t j, uint32_t n, bool& rej) {
+  const uint32_t bound = n - j;
+  const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
+  const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
+  const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
+  rej = static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound;
+  return j + static_cast<uint32_t>(u >> 32);
+}
+__global__ void __launch_bounds__(256) k_giant_count(const HeavyRow* rows, int* flags, uint64_t root, int direct,
+                                                     int wlog, int nwin, uint32_t* hist /*[nwin][ctas]*/) {
+  __shared__ uint32_t sh[256];
   const HeavyRow h = rows[0];
   const uint64_t state = direct ? root : fork64(root, h.row);
-  const uint32_t jend = min(h.b, w1);
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jend; j += gridDim.x * blockDim.x) {
-    const uint32_t bound = h.n - j;
-    const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
-    const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x)) * bound;
-    const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
-    if (static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound) flags[0] = 1;
-    const uint32_t r = j + static_cast<uint32_t>(u >> 32);
-    if (r >= w0 && r < w1 && r != j) {
-      atomicMax(&scratch[h.beg + r], j + 1);
-      if (r < h.b) atomicOr(&tb[r >> 5], 1u << (r & 31u));  // head position targeted: T[r] != 0
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t per = (h.b + gridDim.x - 1) / gridDim.x;
+  const uint32_t j0 = blockIdx.x * per, j1 = min(h.b, j0 + per);
+  bool any_rej = false;
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    bool rej;
+    const uint32_t r = giant_draw(state, j, h.n, rej);
+    any_rej |= rej;
+    if (r != j) atomicAdd(&sh[r >> wlog], 1u);
+  }
+  if (any_rej) flags[0] = 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) hist[static_cast<uint64_t>(i) * gridDim.x + blockIdx.x] = sh[i];
+}
+// Pass 2: exclusive scan of hist in (window, CTA) order (one CTA) -> scatter
+// offsets; wbeg[w] = the first pair of window w (wbeg[nwin] = total).
+__global__ void __launch_bounds__(1024) k_giant_scan(uint32_t* hist, uint32_t n, int nwin, int ctas, uint32_t* wbeg) {
+  __shared__ uint32_t part[1024];
+  const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint32_t a = threadIdx.x * per, b = min(n, a + per);
+  uint32_t s = 0;
+  for (uint32_t i = a; i < b; ++i) s += hist[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (uint32_t t = 0; t < blockDim.x; ++t) {
+      const uint32_t v = part[t];
+      part[t] = run;
+      run += v;
     }
+  }
+  __syncthreads();
+  uint32_t run = part[threadIdx.x];
+  for (uint32_t i = a; i < b; ++i) {
+    const uint32_t v = hist[i];
+    hist[i] = run;
+    if (i % ctas == 0) wbeg[i / ctas] = run;
+    run += v;
+  }
+  if (threadIdx.x == blockDim.x - 1) wbeg[nwin] = run;
+}
+// Pass 3: the same draws again, scattered as (r, j + 1) into their window's bucket.
+__global__ void __launch_bounds__(256) k_giant_scatter(const HeavyRow* rows, uint64_t root, int direct, int wlog,
+                                                       int nwin, const uint32_t* hist, uint2* pairs) {
+  __shared__ uint32_t cur[256];
+  const HeavyRow h = rows[0];
+  const uint64_t state = direct ? root : fork64(root, h.row);
+  for (int i = threadIdx.x; i < nwin; i += blockDim.x) cur[i] = hist[static_cast<uint64_t>(i) * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const uint32_t per = (h.b + gridDim.x - 1) / gridDim.x;
+  const uint32_t j0 = blockIdx.x * per, j1 = min(h.b, j0 + per);
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    bool rej;
+    const uint32_t r = giant_draw(state, j, h.n, rej);
+    if (r != j) pairs[atomicAdd(&cur[r >> wlog], 1u)] = make_uint2(r, j + 1);
+  }
+}
+// Pass 4 (one launch per window): T[r] = max(T[r], j + 1) in L2, and the
+// head-position bitmap tb (r < b: T[r] != 0).
+__global__ void k_giant_apply(const HeavyRow* rows, const uint2* pairs, const uint32_t* wbeg, int w,
+                              uint32_t* scratch, uint32_t* tb) {
+  const HeavyRow h = rows[0];
+  const uint32_t p0 = wbeg[w], p1 = wbeg[w + 1];
+  for (uint32_t i = p0 + blockIdx.x * blockDim.x + threadIdx.x; i < p1; i += gridDim.x * blockDim.x) {
+    const uint2 q = pairs[i];
+    atomicMax(&scratch[h.beg + q.x], q.y);
+    if (q.x < h.b) atomicOr(&tb[q.x >> 5], 1u << (q.x & 31u));
   }
 }
 
@@ -887,6 +955,8 @@ struct HeavyPlan {
   uint32_t* bits = nullptr;       // per giant slice: tb and rb bitmaps over [0, b)
   std::vector<uint64_t> bit_off;  // word offset of giant slice i's tb (rb follows)
   uint64_t bit_words = 0;
+  uint2* pairs = nullptr;     // bucketed draws of one giant slice (b_max pairs)
+  uint32_t* ghist = nullptr;  // [windows][kGiantCtas] histograms / scatter offsets, then wbeg
 };
 // slice length above which the bitmap path runs / the draw window (entries),
 // from the context's tuning (log2, validated to [16, 30] by ntcb_set_tuning)
@@ -941,6 +1011,17 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       pl.bit_words += 2 * ((static_cast<uint64_t>(h.b) + 31) / 32);
     }
     if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * pl.bit_words));
+    if (!pl.giant.empty()) {
+      uint64_t bmax = 0, nmax = 0;
+      for (const HeavyRow& h : pl.giant) {
+        bmax = std::max<uint64_t>(bmax, h.b);
+        nmax = std::max<uint64_t>(nmax, h.n);
+      }
+      const uint64_t nwin = (nmax + heavy_window(ctx) - 1) / heavy_window(ctx);
+      if (nwin > 256) fail(NTCB_EINVAL, "sampler: more than 256 draw windows in one slice");
+      NTCB_CUDA(cudaMalloc(&pl.pairs, sizeof(uint2) * std::max<uint64_t>(bmax, 1)));
+      NTCB_CUDA(cudaMalloc(&pl.ghist, sizeof(uint32_t) * (nwin * kGiantCtas + nwin + 1)));
+    }
     if (!hr.empty()) {
       NTCB_CUDA(cudaMalloc(&pl.rows, sizeof(HeavyRow) * (hr.size() + 1)));
       NTCB_CUDA(cudaMemcpy(pl.rows, hr.data(), sizeof(HeavyRow) * hr.size(), cudaMemcpyHostToDevice));
@@ -950,7 +1031,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   const uint32_t nh = it->second.n;
   if (nh == 0) return 0;
   if (nh > 65535) fail(NTCB_EINVAL, "sampler: more than 65535 heavy slices in one call");
-  if (!ctx->perm_scratch) fail(NTCB_ECUDA, "sampler: heavy slices need the per-entry scratch");
+  if (!view_scratch(ctx, mode)) fail(NTCB_ECUDA, "sampler: heavy slices need the per-entry scratch");
   if (ctx->heavy_flags_n < nh) {
     if (ctx->heavy_flags) cudaFree(ctx->heavy_flags);
     NTCB_CUDA(cudaMalloc(&ctx->heavy_flags, sizeof(int) * nh));
@@ -969,7 +1050,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
   };
   const dim3 gz(gx(maxn), nh);
-  k_heavy_zero<<<gz, 256, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags);
+  k_heavy_zero<<<gz, 256, 0, stream>>>(d, view_scratch(ctx, mode), ctx->heavy_flags);
   const uint32_t n_reg = it->second.n_reg;
   int launches = 2;  // zero, exact
   const HeavyPlan& hp = it->second;
@@ -986,30 +1067,36 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   };
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
-    k_heavy_draw<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->perm_scratch,
+    k_heavy_draw<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
                                                                           ctx->heavy_flags + c.r0, root, direct);
     ++launches;
   }
   if (hp.bit_words) NTCB_CUDA(cudaMemsetAsync(hp.bits, 0, sizeof(uint32_t) * hp.bit_words, stream));
   for (size_t i = 0; i < hp.giant.size(); ++i) {
     const HeavyRow& h = hp.giant[i];
-    const uint32_t W = heavy_window(ctx);
-    for (uint64_t w0 = 0; w0 < h.n; w0 += W) {
-      const uint64_t w1 = std::min<uint64_t>(h.n, w0 + W);
-      const uint64_t jend = std::min<uint64_t>(h.b, w1);
+    const int wlog = ctx->tune.heavy_win_log2;
+    const int nwin = static_cast<int>((static_cast<uint64_t>(h.n) + (1ull << wlog) - 1) >> wlog);
+    const HeavyRow* dr = d + n_reg + i;
+    uint32_t* wbeg = hp.ghist + static_cast<uint64_t>(nwin) * kGiantCtas;
+    k_giant_count<<<kGiantCtas, 256, 0, stream>>>(dr, ctx->heavy_flags + n_reg + i, root, direct, wlog, nwin,
+                                                  hp.ghist);
+    k_giant_scan<<<1, 1024, 0, stream>>>(hp.ghist, static_cast<uint32_t>(nwin) * kGiantCtas, nwin, kGiantCtas,
+                                         wbeg);
+    k_giant_scatter<<<kGiantCtas, 256, 0, stream>>>(dr, root, direct, wlog, nwin, hp.ghist, hp.pairs);
+    launches += 3;
+    for (int w = 0; w < nwin; ++w) {
+      const uint64_t approx = h.b / nwin + 1;  // grid sizing only
       const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
-          1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (jend + 256 * per - 1) / (256 * per))));
-      k_heavy_draw_win<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->perm_scratch, ctx->heavy_flags + n_reg + i, root,
-                                              direct, static_cast<uint32_t>(w0), static_cast<uint32_t>(w1),
-                                              hp.bits + hp.bit_off[i]);
+          1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (approx + 256 * per - 1) / (256 * per))));
+      k_giant_apply<<<g, 256, 0, stream>>>(dr, hp.pairs, wbeg, w, view_scratch(ctx, mode), hp.bits + hp.bit_off[i]);
       ++launches;
     }
   }
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
     k_heavy_tail<<<dim3(gxc(c, (c.mx + 1) / 2 / kTailIlp), c.cnt), 256, 0, stream>>>(
-        d + c.r0, ctx->perm_scratch, ctx->heavy_flags + c.r0, mask);
-    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->perm_scratch,
+        d + c.r0, view_scratch(ctx, mode), ctx->heavy_flags + c.r0, mask);
+    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
                                                                           ctx->heavy_flags + c.r0, mask);
     launches += 2;
   }
@@ -1019,12 +1106,12 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
         1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (h.n / 2 + 256 * per - 1) / (256 * per))));
     const uint32_t* tb = hp.bits + hp.bit_off[i];
     uint32_t* rb = hp.bits + hp.bit_off[i] + (static_cast<uint64_t>(h.b) + 31) / 32;
-    k_heavy_tail_big<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->perm_scratch, ctx->heavy_flags + n_reg + i, mask,
+    k_heavy_tail_big<<<g, 256, 0, stream>>>(d + n_reg + i, view_scratch(ctx, mode), ctx->heavy_flags + n_reg + i, mask,
                                             tb, rb);
     k_heavy_head_big<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->heavy_flags + n_reg + i, mask, rb);
     launches += 2;
   }
-  k_heavy_exact<<<nh, 32, 0, stream>>>(d, ctx->perm_scratch, ctx->heavy_flags, mask, root, direct);
+  k_heavy_exact<<<nh, 32, 0, stream>>>(d, view_scratch(ctx, mode), ctx->heavy_flags, mask, root, direct);
   NTCB_CUDA(cudaGetLastError());
   return launches;
 }
@@ -1034,6 +1121,8 @@ void drop_heavy(ntcb_context* ctx) {
   for (auto& kv : ctx_cache<HeavyPlans>(ctx, kCacheHeavy)) {
     if (kv.second.rows) cudaFree(kv.second.rows);
     if (kv.second.bits) cudaFree(kv.second.bits);
+    if (kv.second.pairs) cudaFree(kv.second.pairs);
+    if (kv.second.ghist) cudaFree(kv.second.ghist);
   }
   ctx_cache_free<HeavyPlans>(ctx, kCacheHeavy);
 }
@@ -1056,7 +1145,7 @@ int launch_sample(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mo
   a.counters = ctx->counters;
   a.dbg_picks = dbg_picks;
   a.dbg_off = dbg_off;
-  a.gscratch = ctx->perm_scratch;
+  a.gscratch = view_scratch(ctx, mode);
   a.direct = direct;
 
   // Shared memory per warp: perm sized to the largest slice (u16 when the

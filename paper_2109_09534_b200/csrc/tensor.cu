@@ -184,16 +184,15 @@ void free_views(ntcb_context* ctx) {
     DeviceView& v = ctx->views[m];
     if (v.off) cudaFree(v.off);
     for (auto& o : v.oth)
-      if (o) cudaFree(o);
-    if (v.val) cudaFree(v.val);
+      if (o) cudaFree(o + v.a_lo);
+    if (v.val) cudaFree(v.val + v.a_lo);
+    for (auto& b : ctx->mask[m]) {
+      if (b) cudaFree(b + (v.a_lo >> 5));
+      b = nullptr;
+    }
     delete[] v.h_off;
     v = DeviceView{};
   }
-  for (auto& mm : ctx->mask)
-    for (auto& b : mm) {
-      if (b) cudaFree(b);
-      b = nullptr;
-    }
   ctx->mask_words = 0;
   if (ctx->partial) cudaFree(ctx->partial);
   ctx->partial = nullptr;
@@ -285,6 +284,9 @@ void build_views(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nn
   for (int m = 0; m < order; ++m) {
     DeviceView& v = ctx->views[m];
     v.rows = dims[m];
+    v.row_lo = 0;
+    v.row_hi = dims[m];
+    v.a_lo = 0;
     NTCB_CUDA(cudaMalloc(&v.off, sizeof(uint64_t) * (v.rows + 1)));
     for (int k = 0; k < order - 1; ++k) NTCB_CUDA(cudaMalloc(&v.oth[k], sizeof(uint32_t) * (nnz + kViewPad)));
     NTCB_CUDA(cudaMalloc(&v.val, sizeof(float) * (nnz + kViewPad)));

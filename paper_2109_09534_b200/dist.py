@@ -3,12 +3,16 @@ sharded across ranks, an all-gather of the updated factor after every mode
 update.
 
 * Rows are independent within a mode update and every row's stream is keyed
-  by (sweep, mode, inner iteration, row) -- never by rank (nmc.cpp:231-236) --
-  so results are bit-identical for any number of GPUs.
+  by (sweep, mode, inner iteration, row) -- never by rank (nmc.cpp:231-236);
+  long rows are cut into the same segments whatever the row range
+  (update.cu segment_length), so results are bit-identical for any number of
+  GPUs (tests/test_gpu_invariance.py, test_gpu_slabs.py).
 * Each rank updates a contiguous row range chosen by prefix sums of work
-  (sampled entries + a per-row overhead), not equal row counts, and holds
-  replicas of every factor; only A^(n) is exchanged (I_n x ld fp32), Y stays
-  local (it is reset at every S_NMC call, nmc.cpp:212-215).
+  (sampled entries + a per-row overhead), not equal row counts, keeps only
+  that slab of every mode view on its device (ntcb_view_keep_rows: ~1/N of
+  the views per GPU) and holds replicas of every factor; only A^(n) is
+  exchanged (I_n x ld fp32), Y stays local (it is reset at every S_NMC call,
+  nmc.cpp:212-215).
 * The exchange is a torch.distributed all-gather (NCCL over NVLink on GPUs,
   gloo in the CPU tests) of padded shards into the resident factor memory.
 """
@@ -143,7 +147,8 @@ class ShardedSweep:
     (exchange="p2p", the default when every GPU can map every other's
     memory) or by an NCCL all-gather of the shards (exchange="gather")."""
 
-    def __init__(self, ctx, cfg, rank: int, world: int, group=None, exchange: str = "auto"):
+    def __init__(self, ctx, cfg, rank: int, world: int, group=None, exchange: str = "auto",
+                 slab: bool = True):
         import os
 
         import torch
@@ -152,6 +157,10 @@ class ShardedSweep:
         order, dims, _ = ctx.info()
         self.dims = dims
         self.bounds = [partition_rows(ctx.view_offsets(m), cfg.c, world) for m in range(order)]
+        if slab:  # this rank's rows only: ~1/N of every view stays on the device
+            for m in range(order):
+                ctx.view_keep_rows(m, *self.bounds[m][rank])
+        self.view_bytes = [ctx.view_resident(m)[2] for m in range(order)]
         self.A = [factor_tensor(ctx, m, dims[m]) for m in range(order)]
         st = torch.cuda.current_stream()
         if st.cuda_stream == 0:  # legacy default stream has no handle; use a real one
@@ -194,6 +203,18 @@ class ShardedSweep:
     def sweep(self, k: int, seed: int) -> None:
         for m in range(len(self.dims)):
             self.sweep_mode(k, m, seed)
+
+    def metrics(self):
+        """(sse, sum x^2, sum ||U||^2) of the whole tensor: every rank's
+        partial sums over its mode-0 slab, all-reduced (the factors are
+        replicated, so the regulariser is taken from this rank)."""
+        import torch
+        import torch.distributed as tdist
+        sse, sx, reg = self.ctx.metrics()
+        t = torch.tensor([sse, sx], dtype=torch.float64, device="cuda" if self.nccl else "cpu")
+        if tdist.is_available() and tdist.is_initialized():
+            tdist.all_reduce(t, group=self.group)
+        return float(t[0]), float(t[1]), reg
 
     def local_sampled(self, m: int) -> int:
         r0, r1 = self.bounds[m][self.rank]

@@ -281,6 +281,17 @@ class Context:
                                            oth.ctypes.data_as(u32p), val.ctypes.data_as(f32p)))
         return off - off[0], oth[: n * (order - 1)].reshape(n, order - 1), val[:n]
 
+    def view_keep_rows(self, mode, row_begin, row_end):
+        """Slab storage (ntcb_view_keep_rows): only rows [row_begin, row_end)
+        of view `mode` stay on the device."""
+        check(self.L.ntcb_view_keep_rows(self.h, mode, row_begin, row_end))
+
+    def view_resident(self, mode):
+        """(row_begin, row_end, device bytes) of the resident part of a view."""
+        a, b, n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(self.L.ntcb_view_resident(self.h, mode, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     def set_stream(self, stream_ptr):
         check(self.L.ntcb_set_stream(self.h, C.c_void_p(stream_ptr)))
 
