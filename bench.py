@@ -76,9 +76,9 @@ def l2_note(c, l2_bytes=126 * 2**20):
             f"not the headline")
 
 
-def update_kernel_name(R, order):
+def update_kernel_name(R, order, ld):
     """The update kernel update.cu:launch_ld dispatches to."""
-    if 25 <= R <= 32 and order in (3, 4):
+    if (25 <= R <= 32 or (ld == 32 and 9 <= R <= 24)) and order in (3, 4):
         return "k_update_tc NAT (natural-layout gathers + tensor-core Hessian + power method + step)"
     if R <= 31 and order <= 4:
         return "k_update_tc (gradient + tensor-core Hessian + power method + step)"
@@ -494,7 +494,7 @@ def run_ours(args, cfgd, cid):
             "sec_per_ao_iteration": ms / args.steps / 1000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": update_kernel_name(R, order),
+                         "kernel": update_kernel_name(R, order, ctx.factor_device_ptr(0)[1]),
                          "alg_bytes_per_launch": per_launch_bytes,
                          "gathers_counted_in_modes": gather_modes,
                          "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)

@@ -429,6 +429,7 @@ void free_factors(ntcb_context* ctx) {
     ctx->A[m] = ctx->Y[m] = nullptr;
   }
   ctx->rank = ctx->ld = 0;
+  ctx->nat_padded = false;
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) ctx->n_peers[m] = 0;
 }
 
@@ -441,6 +442,12 @@ void alloc_factors(ntcb_context* ctx, uint64_t rank) {
   // row stride: whole 32-byte sectors up to rank 31 (the tensor-core update
   // gathers feature blocks of 8), 16-byte multiples above
   ctx->ld = rank <= 31 ? (rank + 7) / 8 * 8 : (rank + 3) / 4 * 4;
+  // nat_pad: 128-byte rows (one L1 line per gathered row) for the NAT update
+  uint64_t fbytes = 0;
+  for (int m = 0; m < ctx->order; ++m) fbytes += ctx->dims[m] * rank * 4;
+  const bool pad = ctx->tune.nat_pad == 1 || (ctx->tune.nat_pad == -1 && fbytes > (16ull << 20));
+  ctx->nat_padded = pad && rank >= 9 && rank <= 24 && (ctx->order == 3 || ctx->order == 4);
+  if (ctx->nat_padded) ctx->ld = 32;
   for (int m = 0; m < ctx->order; ++m) {
     // + 32 floats: the tensor-core gather of the last row may read past it
     const size_t bytes = sizeof(float) * (ctx->dims[m] * ctx->ld + 32);
@@ -561,6 +568,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
   if (t->heavy_win_log2 < 16 || t->heavy_win_log2 > 30 || t->heavy_big_log2 < 16 || t->heavy_big_log2 > 30)
     fail(NTCB_EINVAL, "tuning: heavy_win_log2 / heavy_big_log2 must be in [16, 30]");
   if (t->host_threads < 0) fail(NTCB_EINVAL, "tuning: host_threads must be >= 0");
+  if (t->nat_pad < -1 || t->nat_pad > 1) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0 or 1");
   collect(ctx, nullptr);  // queued work keeps the plans it was launched with
   ctx->tune = *t;
   drop_plans(ctx);  // plans bake in the heavy-window sizes and the short-row decision
@@ -1170,18 +1178,47 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
     if (!hs.verified[m]) fail(NTCB_EINVAL, "ao_ntc: init factors must be nonnegative");
   collect(ctx, nullptr);
 
+  // Device-resident loop (ao.cpp:75-133): the entries a sweep accesses are
+  // known on the host before it runs (sum of floor(c n_p), nmc.cpp:36-40),
+  // so the budget and zero-progress checks need no synchronisation; sweeps
+  // are enqueued back to back and the host waits only where a record needs
+  // device data (eval_metrics, an observer) and at the end.  Records without
+  // device data take their wall_seconds from a CUDA event recorded after
+  // their sweep (time since t0 at which the sweep finished on the device).
   std::vector<ntcb_metrics_record> hist;
+  std::vector<std::pair<size_t, cudaEvent_t>> deferred;  // (record index, end-of-sweep event)
+  struct EvFree {
+    std::vector<std::pair<size_t, cudaEvent_t>>& d;
+    cudaEvent_t base = nullptr;
+    ~EvFree() {
+      for (auto& x : d) cudaEventDestroy(x.second);
+      if (base) cudaEventDestroy(base);
+    }
+  } evfree{deferred};
   uint64_t accessed = 0;
   const auto t0 = std::chrono::steady_clock::now();
+  NTCB_CUDA(cudaEventCreate(&evfree.base));
+  NTCB_CUDA(cudaEventRecord(evfree.base, ctx->stream));
+  const double base_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const bool sync_records = cfg->eval_metrics || observer != nullptr;
   auto push = [&]() {
     ntcb_metrics_record r{};
     r.entries_accessed = accessed;
     if (ctx->nnz == 0) fail(NTCB_EINVAL, "epoch_fraction: empty observation set");
     r.epoch = static_cast<double>(accessed) / static_cast<double>(ctx->nnz);
-    r.wall_seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r.objective = std::nan("");
     r.rel_error = std::nan("");
+    if (!sync_records) {
+      cudaEvent_t e;
+      NTCB_CUDA(cudaEventCreate(&e));
+      NTCB_CUDA(cudaEventRecord(e, ctx->stream));
+      deferred.emplace_back(hist.size(), e);
+      hist.push_back(r);
+      return;
+    }
+    collect(ctx, nullptr);  // queued sweeps done, first row failure reported
+    r.wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (cfg->eval_metrics) {
       double sse, sx, reg;
       device_metrics(ctx, &sse, &sx, &reg);
@@ -1201,13 +1238,18 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
     uint64_t st = 0;
     for (int i = 0; i < ctx->order; ++i)
       st += enqueue_snmc_owned(ctx, i, 0, ctx->dims[i], n, ntcb_sweep_stream_state(cfg->seed, k, i));
-    collect(ctx, nullptr);
     if (st == 0) break;
     accessed += st;
     last_recorded = ((k + 1) % static_cast<uint64_t>(cfg->metrics_every) == 0);
     if (last_recorded) push();
   }
   if (!last_recorded) push();
+  collect(ctx, nullptr);  // the remaining sweeps; a row failure throws here
+  for (auto& x : deferred) {
+    float ms = 0.f;
+    NTCB_CUDA(cudaEventElapsedTime(&ms, evfree.base, x.second));
+    hist[x.first].wall_seconds = base_s + 1e-3 * ms;
+  }
   if (n_history) *n_history = hist.size();
   if (history)
     for (uint64_t i = 0; i < hist.size() && i < max_history; ++i) history[i] = hist[i];

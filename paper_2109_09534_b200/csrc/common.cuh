@@ -110,6 +110,7 @@ inline ntcb_tuning default_tuning() {
   t.heavy_win_log2 = 24;
   t.heavy_big_log2 = 24;
   t.host_threads = 0;
+  t.nat_pad = -1;
   return t;
 }
 
@@ -136,6 +137,7 @@ struct ntcb_context {
   // factors
   uint64_t rank = 0;
   uint64_t ld = 0;
+  bool nat_padded = false;  // 128-byte rows below rank 25: the update runs the NAT kernel
   float* A[NTCB_MAX_ORDER] = {};
   float* peerA[NTCB_MAX_ORDER][7] = {};  // replicas of A[m] on other GPUs (fused exchange)
   int n_peers[NTCB_MAX_ORDER] = {};

@@ -1485,11 +1485,21 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // view (a property of the mode, not of a shard: the instantiation must not
   // depend on the partition) -- per-row latencies dominate there
   const bool short_rows = mode_short_rows(ctx, a.mode, a.c);
-  if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && a.rank >= 25 && (a.no == 2 || a.no == 3)) {
-    // ranks 25-32: natural-layout gathers through a shared tile into the
-    // tensor-core Gram (w on the CUDA cores)
+  if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && (a.rank >= 25 || ctx->nat_padded) &&
+      (a.no == 2 || a.no == 3)) {
+    // ranks 25-32 (and 9-24 with nat_pad's 128-byte rows): natural-layout
+    // gathers through a shared tile into the tensor-core Gram (w on the CUDA
+    // cores); P = feature blocks of 8 (no x column)
     const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true)) * 4 * kWarps;
-    launches += a.no == 2 ? launch_items_tc<4, 2, true>(ctx, a, pl, ts) : launch_items_tc<4, 3, true>(ctx, a, pl, ts);
+    const int pn = (a.rank + 7) / 8;
+    if (a.no == 2)
+      launches += pn == 2 ? launch_items_tc<2, 2, true>(ctx, a, pl, ts)
+                : pn == 3 ? launch_items_tc<3, 2, true>(ctx, a, pl, ts)
+                          : launch_items_tc<4, 2, true>(ctx, a, pl, ts);
+    else
+      launches += pn == 2 ? launch_items_tc<2, 3, true>(ctx, a, pl, ts)
+                : pn == 3 ? launch_items_tc<3, 3, true>(ctx, a, pl, ts)
+                          : launch_items_tc<4, 3, true>(ctx, a, pl, ts);
   } else if (pl.n_items && short_rows && a.no == 2 && (P == 2 || P == 3) && !g_tc_off) {
     // order 3, ranks 8-23, short rows on average (Zipf tails: configs 3 and
     // 5): the variant that stages each row's A and Y with its first batch

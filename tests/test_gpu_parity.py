@@ -379,6 +379,31 @@ def test_ao_zero_progress_and_budget(ntc):
     assert len(res.history) == 1
 
 
+def test_ao_ntc_deferred_sync_records(ntc):
+    """ntcb_ao_ntc without metrics or observer enqueues its sweeps back to
+    back (one synchronisation at the end): the history still has one record
+    per metrics_every sweeps with exact entry counts and increasing wall
+    times, and the factors equal the same sweeps queued one by one."""
+    import paper_2109_09534_b200 as P
+    ctx = P.Context(0)
+    ctx.synth_uniform([300, 200, 100], 400_000, 5, 0.01, 21)
+    ctx.random_factors(6, 7)
+    per = sum(int(np.floor(0.5 * np.diff(ctx.view_offsets(m).astype(np.float64))).sum()) for m in range(3))
+    cfg = P.AoConfig(rank=6, c=0.5, max_epochs=per * 7 / ctx.info()[2] - 1e-9, seed=11, eval_metrics=False,
+                     metrics_every=2)
+    hist = ctx.ao_ntc(cfg)
+    assert [h.entries_accessed for h in hist] == [0, 2 * per, 4 * per, 6 * per, 7 * per]
+    w = [h.wall_seconds for h in hist]
+    assert all(b > a for a, b in zip(w, w[1:]))
+    A = [ctx.get_factor(m)[0] for m in range(3)]
+    ctx.random_factors(6, 7)
+    for k in range(7):
+        ctx.sweep_async(k, P.NmcConfig(c=0.5), 11)
+    assert ctx.collect() == 7 * per
+    for m in range(3):
+        np.testing.assert_array_equal(ctx.get_factor(m)[0], A[m])
+
+
 # ---------------------------------------------------------------- trajectory at scale
 def test_trajectory_20_iterations_vs_oracle(ntc, orc):
     """Free-running 20 AO iterations on a 1%-dense 160^3 tensor (cfg-1 style,

@@ -59,6 +59,20 @@ __global__ void __launch_bounds__(256, 2) k(const float* __restrict__ U, const u
         v[h] = __ldg(reinterpret_cast<const float4*>(b) + (lane & 7));
       }
       acc += v[0].x * v[0].y + v[0].z * v[0].w + v[1].x * v[1].y + v[1].z * v[1].w;
+    } else if (V == 7) {  // quad fragment layout: lane (g,t) reads picks 2t+q, float4 at 4g (8 strided lanes per row)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float* b = U + (size_t)r[2 * t + q] * LD;
+        float4 v = __ldg(reinterpret_cast<const float4*>(b + 4 * g));
+        acc += v.x * v.y + v.z * v.w;
+      }
+    } else if (V == 8) {  // quad, pick t + 4q (fragment k-index order)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float* b = U + (size_t)r[t + 4 * q] * LD;
+        float4 v = __ldg(reinterpret_cast<const float4*>(b + 4 * g));
+        acc += v.x * v.y + v.z * v.w;
+      }
     } else if (V == 4) {  // natural float2: 12 lanes per row (2.67 rows per instr) -> 16 lanes per row, 2 rows per instr
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
@@ -109,6 +123,8 @@ int main() {
   run(k<2, 32>, "natural ld32 float4");
   run(k<5, 32>, "natural ld32 float4 + 8 SHFL");
   run(k<6, 32>, "natural ld32 float4 (V5 w/o SHFL)");
+  run(k<7, 32>, "quad ld32 (lane g,t: pick 2t+q, float4 4g)");
+  run(k<8, 32>, "quad ld32 (lane g,t: pick t+4q, float4 4g)");
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
