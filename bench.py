@@ -294,6 +294,142 @@ def cpu_baseline_sample(cfgd, cid):
 
 
 # ---------------------------------------------------------------------------
+def roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches, smp_ms_step,
+                   upd_ms_step):
+    """Roofline of the dominant kernel (one mode update: k_update_tc + the
+    split-row finalisation), SURVEY.md §8(d).
+    achieved = algorithmic bytes per launch / this run's average launch time
+    (CUDA events on the library stream), against the measured HBM peak.
+    Algorithmic bytes = 4N B per sampled entry (value + N-1 coordinates) +
+    (16R + 8) B per processed row; factor-row gathers are NOT counted (they
+    are L1/L2 traffic at configs 1-4; at config 5 they partly reach DRAM and
+    are reported separately as gather_bytes_if_uncached).
+    traffic / dram_frac / lsu_util: from the committed ncu --set full capture
+    of the same kernel and config (profiles/ncu_traffic_cfgN.json, source
+    named; not measured inside this run): dram_frac = ncu DRAM bytes per
+    launch / this run's launch time / peak."""
+    from paper_2109_09534_b200.dist import blocksizes
+    dims, R = cfgd["dims"], cfgd["R"]
+    N = len(dims)
+    hbm, peak_src = peaks()
+    alg_bytes = 4 * N * full + (16 * R + 8) * rows_processed  # per sweep
+    gathers = (N - 1) * 4 * R * full
+    per_launch = alg_bytes / N
+    avg_s = (upd_ms / max(upd_launches, 1)) / 1000.0
+    achieved = per_launch / avg_s / 1e9
+    alg_flops = 2 * ((N - 2) * R + 3 * R + R * (R + 1) // 2) * full + 8 * R * rows_processed
+    flops_launch = alg_flops / N
+    fp32_peak = 70.8
+    out = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+           "traffic": None, "peak_source": peak_src,
+           "kernel": update_kernel_name(R, N, ctx.factor_device_ptr(0)[1]),
+           "alg_bytes_per_launch": per_launch,
+           "gather_bytes_if_uncached_per_launch": gathers / N,
+           "avg_launch_ms": avg_s * 1000.0,
+           # side-stream spans include queueing behind the update: not busy time
+           "sampler_span_ms_per_step": smp_ms_step, "update_ms_per_step": upd_ms_step,
+           "compute": {"alg_flops_per_launch": flops_launch, "achieved_tflops": flops_launch / avg_s / 1e12,
+                       "fp32_peak_tflops": fp32_peak,
+                       "fp32_peak_source": "measured FFMA, tools/microbench/hmma.cu",
+                       "frac_fp32": flops_launch / avg_s / 1e12 / fp32_peak},
+           "binding_unit": None}
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        t = tj.get("dram_bytes_per_launch")
+        out["traffic"] = t
+        out["dram_frac"] = (t / avg_s / 1e9 / hbm) if t else None
+        out["binding_unit"] = {"unit": tj.get("limiter_unit"), "lsu_wavefront_util": tj.get("util"),
+                               "lsu_wavefronts_per_sampled_entry": tj.get("lsu_wavefronts_per_unit"),
+                               "ncu_dram_util": tj.get("dram_util"), "source": tj.get("source"),
+                               "measured_in_this_run": False}
+    return out
+
+
+def sub_record(cid, steps=3, warmup=3, tune=()):
+    """A compact 1-GPU measurement of another BASELINE config for the main
+    bench line (device value, e2e through ntcb_s_nmc_host, roofline)."""
+    import torch
+    import paper_2109_09534_b200 as P
+    from paper_2109_09534_b200.dist import blocksizes
+    cfgd = CONFIGS[cid]
+    dims, R = cfgd["dims"], cfgd["R"]
+    order = len(dims)
+    stream = torch.cuda.current_stream()
+    ctx = P.Context(torch.cuda.current_device())
+    try:
+        if tune:
+            ctx.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in tune)})
+        ctx.set_stream(stream.cuda_stream)
+        generate(ctx, cfgd, cid)
+        ctx.random_factors(R, SEED_SOLVER)
+        cfg = P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1)
+        offs = [ctx.view_offsets(m) for m in range(order)]
+        full = sum(int(blocksizes(o, cfg.c).sum()) for o in offs)
+        rows_processed = sum(int((blocksizes(o, cfg.c) > 0).sum()) for o in offs)
+        for k in range(warmup):
+            ctx.sweep_async(k, cfg, SEED_SOLVER)
+        ctx.collect()
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(warmup, warmup + steps):
+            ctx.sweep_async(k, cfg, SEED_SOLVER)
+        e1.record()
+        torch.cuda.synchronize()
+        assert ctx.collect() == full * steps
+        upd_ms, smp_ms, launches, upd_launches = ctx.profile_read()
+        ctx.profile(False)
+        ms = e0.elapsed_time(e1)
+        e2e = e2e_host(ctx, dims, cfg, steps, P)
+        return {"workload": workload_name(cid, cfgd), "value": full * steps / (ms / 1000.0), "unit": UNIT,
+                "ms_per_step": ms / steps, "sec_per_ao_iteration": ms / steps / 1000.0, "steps": steps,
+                "warmup": warmup, "sampled_per_ao_iteration": full, "l2": l2_note(cfgd),
+                "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches,
+                                           smp_ms / steps, upd_ms / steps)}
+    finally:
+        ctx.close()
+
+
+def e2e_host(ctx, dims, cfg, steps, P):
+    """End to end through the host-buffer C-ABI (ntcb_s_nmc_host): per mode,
+    host double a_init -> device, S_NMC, A and Y -> host double; wall clock
+    (>= the device time) around the whole loop."""
+    import torch
+    order = len(dims)
+    # page-locked host buffers (the e2e contract's pinned host memory): the
+    # library converts fp64 <-> fp32 on the device and copies straight to them
+    Fh = [P.pinned_like(ctx.get_factor(m)[0]) for m in range(order)]
+    outs = [(P.pinned_like(np.zeros_like(f)), P.pinned_like(np.zeros_like(f))) for f in Fh]
+    ld = ctx.factor_device_ptr(0, 0)[1]
+    h2d = sum(d * ld * 4 for d in dims)
+    d2h = 2 * h2d
+    full = 0
+    for m in range(order):  # untimed warm-up call per mode (device io buffers, plans)
+        ctx.s_nmc_host(m, Fh[m], outs[m][0], outs[m][1], cfg, P.sweep_stream(SEED_SOLVER, 9_999, m).state)
+        Fh[m][...] = outs[m][0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record()
+    for k in range(steps):
+        for m in range(order):
+            full += ctx.s_nmc_host(m, Fh[m], outs[m][0], outs[m][1], cfg,
+                                   P.sweep_stream(SEED_SOLVER, 10_000 + k, m).state)
+            Fh[m] = outs[m][0]
+    ee1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    e_ms = max(ee0.elapsed_time(ee1), 1000.0 * wall)
+    return {"value": full / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "ntcb_s_nmc_host per mode: pinned host double a_init -> device (fp64 -> fp32 on the device), "
+                    "S_NMC, A and Y back to pinned host double"}
+
+
+# ---------------------------------------------------------------------------
 def run_ours(args, cfgd, cid):
     import torch
     import torch.distributed as dist
@@ -376,69 +512,13 @@ def run_ours(args, cfgd, cid):
         assert acc == total_sampled, (acc, total_sampled)
     value = total_sampled / (ms / 1000.0)
 
-    # ---- roofline of the dominant kernel (k_update) ----------------------------
-    hbm, peak_src = peaks()
-    N = order
-    alg_bytes = 4 * N * full + (16 * R + 8) * rows_processed  # per sweep, SURVEY.md §8(d)
-    # + (N-1) 4R B of factor-row gathers per sampled nnz in the modes whose
-    # other factors exceed L2 (config 5 only)
-    gather_modes = []
-    for m in range(order):
-        other = sum(dims[q] * R * 4 for q in range(order) if q != m)
-        if other > 126 * 2**20:
-            alg_bytes += (N - 1) * 4 * R * int(blocksizes(offs[m], cfg.c).sum())
-            gather_modes.append(m)
-    per_launch_bytes = alg_bytes / order
-    avg_upd_s = (upd_ms / max(upd_launches, 1)) / 1000.0
-    achieved = per_launch_bytes / avg_upd_s / 1e9
-    # compute side: reference-formulation FLOPs per sampled nnz
-    # 2[(N-2)R + 3R + R(R+1)/2] plus ~8R per processed row (power iterations not
-    # counted), against the CUDA-core FP32 peak measured on this pool
-    # (tools/microbench/hmma.cu: 70.8 TFLOP/s FFMA)
-    alg_flops = 2 * ((N - 2) * R + 3 * R + R * (R + 1) // 2) * full + 8 * R * rows_processed
-    flops_launch = alg_flops / order
-    fp32_peak = 70.8
-    compute = {"alg_flops_per_launch": flops_launch,
-               "achieved_tflops": flops_launch / avg_upd_s / 1e12,
-               "fp32_peak_tflops": fp32_peak, "fp32_peak_source": "measured FFMA, tools/microbench/hmma.cu",
-               "frac_fp32": flops_launch / avg_upd_s / 1e12 / fp32_peak}
-    limiter = {"unit": f"L1/LSU data pipe ({N - 1} factor-row gathers per sampled nnz; Gram on tensor cores)",
-               "util": None, "dram_util": None, "source": None}
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{cid}.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            tj = json.load(f)
-        traffic = tj.get("dram_bytes_per_launch")
-        limiter.update({k: tj.get(k) for k in ("util", "dram_util", "source") if k in tj})
-        if tj.get("limiter_unit"):
-            limiter["unit"] = tj["limiter_unit"]
+    roofline = roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches,
+                              smp_ms / args.steps, upd_ms / args.steps)
 
     # ---- end to end through the host-buffer C-ABI --------------------------------
     e2e = None
     if not distributed:
-        Fh = [np.ascontiguousarray(ctx.get_factor(m)[0]) for m in range(order)]
-        outs = [(np.zeros_like(f), np.zeros_like(f)) for f in Fh]
-        ld = ctx.factor_device_ptr(0, 0)[1]
-        h2d = sum(d * ld * 4 for d in dims)
-        d2h = 2 * h2d
-        t0 = time.perf_counter()
-        ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ee0.record()
-        ne = 0
-        for k in range(args.steps):
-            for m in range(order):
-                ne += ctx.s_nmc_host(m, Fh[m], outs[m][0], outs[m][1], cfg,
-                                     P.sweep_stream(SEED_SOLVER, 10_000 + k, m).state)
-                Fh[m] = outs[m][0]
-        ee1.record()
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        e_ms = max(ee0.elapsed_time(ee1), 1000.0 * wall)
-        e2e = {"value": ne / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h,
-               "path": "ntcb_s_nmc_host per mode: host double a_init -> device, S_NMC, "
-                       "A and Y back to host double"}
+        e2e = e2e_host(ctx, dims, cfg, args.steps, P)
     else:
         # per mode: this rank's a_init rows from pinned host memory -> device,
         # sharded S_NMC + NCCL all-gather, the full updated factor -> host
@@ -492,19 +572,19 @@ def run_ours(args, cfgd, cid):
                        "l2": l2_note(cfgd),
                        "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
             "sec_per_ao_iteration": ms / args.steps / 1000.0,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": update_kernel_name(R, order, ctx.factor_device_ptr(0)[1]),
-                         "alg_bytes_per_launch": per_launch_bytes,
-                         "gathers_counted_in_modes": gather_modes,
-                         "avg_launch_ms": avg_upd_s * 1000.0,  # one mode update (update + finalise kernels)
-                         # side-stream spans include queueing behind the update: not busy time
-                         "sampler_span_ms_per_step": smp_ms / args.steps,
-                         "update_ms_per_step": upd_ms / args.steps,
-                         "compute": compute, "limiter": limiter},
+            "roofline": roofline,
             "clocks": clocks, "gpu_launches": launches,
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if world == 1 and not distributed and cid == 2 and not args.no_sub:
+            # the other BASELINE configs, one GPU each (driver-visible sub-records)
+            ctx.close()
+            out["other_configs"] = {}
+            for c2 in (1, 3, 4, 5):
+                try:
+                    out["other_configs"][f"cfg{c2}"] = sub_record(c2, tune=args.tune)
+                except Exception as e:  # a sub-record never voids the headline line
+                    out["other_configs"][f"cfg{c2}"] = {"error": f"{type(e).__name__}: {e}"}
         print(json.dumps(out), flush=True)
     if distributed:
         dist.destroy_process_group()
@@ -518,6 +598,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sub", action="store_true", help="skip the other configs' sub-records")
     ap.add_argument("--tune", nargs="*", default=[], metavar="K=V",
                     help="ntcb_tuning launch-policy knobs for A/B runs, e.g. --tune split_rows=1")
     args = ap.parse_args()

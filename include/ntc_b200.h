@@ -94,6 +94,10 @@ int ntcb_destroy(ntcb_context* ctx);
  * restores the context's own stream. */
 int ntcb_set_stream(ntcb_context* ctx, void* cuda_stream);
 int ntcb_synchronize(ntcb_context* ctx);
+/* Page-locked host memory (cudaMallocHost) for factor buffers of the
+ * host-buffer entry points; ntcb_host_free releases it. */
+int ntcb_host_alloc(uint64_t bytes, void** out);
+int ntcb_host_free(void* p);
 
 /* ---- tuning (launch policy only; no reference analogue) -----------------
  * Per-context launch choices behind the measured defaults of DESIGN.md §3.
@@ -219,7 +223,11 @@ int ntcb_factor_set_peers(ntcb_context* ctx, int mode, int n, void* const* peer_
 int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc_config* cfg,
                uint64_t rng_state, uint64_t* entries_accessed);
 /* Host-buffer drop-in: a_init in, updated factors[mode] (a_out) and
- * momentum[mode] (y_out) out, all host double; H2D/D2H inside the call. */
+ * momentum[mode] (y_out) out, all host double; H2D/D2H inside the call.
+ * When every buffer is page-locked (e.g. from ntcb_host_alloc) the fp64 <->
+ * fp32 conversion and the nonnegativity check run on the device and the
+ * copies go straight to and from the caller's arrays; otherwise the call
+ * converts on the host through its own pinned staging.  Same results. */
 int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a_out,
                     double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
                     uint64_t* entries_accessed);

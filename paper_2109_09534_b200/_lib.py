@@ -81,6 +81,8 @@ SIGNATURES = {
     "ntcb_destroy": (C.c_int, [C.c_void_p]),
     "ntcb_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ntcb_synchronize": (C.c_int, [C.c_void_p]),
+    "ntcb_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "ntcb_host_free": (C.c_int, [C.c_void_p]),
     "ntcb_tuning_defaults": (None, [C.POINTER(TuningC)]),
     "ntcb_set_tuning": (C.c_int, [C.c_void_p, C.POINTER(TuningC)]),
     "ntcb_get_tuning": (C.c_int, [C.c_void_p, C.POINTER(TuningC)]),

@@ -60,6 +60,10 @@ struct HostState {
   std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, uint64_t> bs_cache;
   float* stage = nullptr;  // pinned fp32 staging for host-buffer factor transfers
   uint64_t stage_n = 0;    // floats
+  void* io_in = nullptr;   // device fp64 a_init / fp32 scratch / fp64 outputs (pinned-buffer path)
+  void* io_f = nullptr;
+  void* io_out = nullptr;
+  uint64_t io_in_cap = 0, io_f_cap = 0, io_out_cap = 0;  // bytes
   bool queued = false;     // work enqueued since the last collect
 };
 HostState& host_of(ntcb_context* ctx) { return *static_cast<HostState*>(ctx->host); }
@@ -179,13 +183,15 @@ int enqueue_sample(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, const 
 // Returns the entries this call will access (also added to the pending
 // count that ntcb_collect hands back).
 uint64_t enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
-                      const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
+                      const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1,
+                      bool y_set = false) {
   const uint64_t ld = ctx->ld;
   cudaStream_t st = ctx->stream;
   if (r1 <= r0) return 0;
-  // A_0 = Y_0 = a_init (nmc.cpp:212-215); A already holds a_init.
-  NTCB_CUDA(cudaMemcpyAsync(ctx->Y[mode] + r0 * ld, ctx->A[mode] + r0 * ld,
-                            sizeof(float) * (r1 - r0) * ld, cudaMemcpyDeviceToDevice, st));
+  // A_0 = Y_0 = a_init (nmc.cpp:212-215); A already holds a_init (y_set: Y too).
+  if (!y_set)
+    NTCB_CUDA(cudaMemcpyAsync(ctx->Y[mode] + r0 * ld, ctx->A[mode] + r0 * ld,
+                              sizeof(float) * (r1 - r0) * ld, cudaMemcpyDeviceToDevice, st));
   const DeviceView& v = ctx->views[mode];
   const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
   for (int l = 0; l < cfg.max_inner; ++l) {
@@ -211,8 +217,9 @@ uint64_t enqueue_snmc(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
 // any other, but its entries are taken out of the pending count again, so a
 // later ntcb_collect still returns exactly the async work queued by the user.
 uint64_t enqueue_snmc_owned(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
-                            const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1) {
-  const uint64_t n = enqueue_snmc(ctx, mode, r0, r1, cfg, rng_state, presampled);
+                            const ntcb_nmc_config& cfg, uint64_t rng_state, int presampled = -1,
+                            bool y_set = false) {
+  const uint64_t n = enqueue_snmc(ctx, mode, r0, r1, cfg, rng_state, presampled, y_set);
   host_of(ctx).pending_accessed -= n;
   return n;
 }
@@ -245,6 +252,7 @@ void collect(ntcb_context* ctx, uint64_t* accessed) {
       fail(NTCB_ERUNTIME, "s_nmc: non-finite gradient at row " + std::to_string(row + 1) +
                               " (mode " + std::to_string(mode + 1) + ")");
     if (kind == 1) fail(NTCB_ERUNTIME, "power_method: non-finite entries in matrix");
+    if (kind == 3) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");  // pinned-buffer path
     fail(NTCB_ERUNTIME, "row_step: step constant below lambda");
   }
   if (accessed) *accessed += pend;
@@ -478,6 +486,73 @@ bool plateau(const std::vector<ntcb_metrics_record>& h, double tol) {
   return true;
 }
 
+// ---- host-buffer S_NMC with page-locked caller buffers: the fp64 <-> fp32
+// conversion runs on the device, the copies go straight between the caller's
+// pinned arrays and the device (no host-side conversion or staging) ----------
+__global__ void k_a_init_in(const double* src, uint64_t rows, int R, int ld, float* dst,
+                            unsigned long long* counters, int mode) {
+  const uint64_t n = rows * static_cast<uint64_t>(ld);
+  bool bad = false;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = q / ld;
+    const int r = static_cast<int>(q - i * ld);
+    float v = 0.f;
+    if (r < R) {
+      const double d = src[i * R + r];
+      bad |= !(d >= 0.0);  // negative or NaN (nmc.cpp:202-210)
+      v = static_cast<float>(d);
+    }
+    dst[q] = v;
+  }
+  // one key for the whole call: row 0, kind 3 ("a_init must be nonnegative")
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicMin(&counters[1], (static_cast<unsigned long long>(mode) << 58) | 3ull);
+}
+// A = Y = a_init, only when every value passed (the update kernels see the
+// error key and do nothing either: A and Y stay untouched, as in the reference)
+__global__ void k_a_init_commit(const float* src, uint64_t n, float* A, float* Y, const unsigned long long* counters) {
+  if (*reinterpret_cast<const volatile unsigned long long*>(&counters[1]) != ~0ull) return;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float v = src[q];
+    A[q] = v;
+    Y[q] = v;
+  }
+}
+__global__ void k_factors_out(const float* A, const float* Y, uint64_t rows, int R, int ld, double* a,
+                              double* y) {
+  const uint64_t n = rows * static_cast<uint64_t>(R);
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = q / R, r = q - i * R;
+    if (a) a[q] = static_cast<double>(A[i * ld + r]);
+    if (y) y[q] = static_cast<double>(Y[i * ld + r]);
+  }
+}
+
+bool pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+template <class T>
+T* io_buffer(void*& buf, uint64_t& cap, uint64_t n) {
+  if (cap < sizeof(T) * n) {
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    cap = 0;
+    NTCB_CUDA(cudaMalloc(&buf, sizeof(T) * n));
+    cap = sizeof(T) * n;
+  }
+  return static_cast<T*>(buf);
+}
+
 }  // namespace
 
 extern "C" {
@@ -532,6 +607,8 @@ int ntcb_destroy(ntcb_context* ctx) {
   cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->own_stream);
   if (host_of(ctx).stage) cudaFreeHost(host_of(ctx).stage);
+  for (void* p : {host_of(ctx).io_in, host_of(ctx).io_f, host_of(ctx).io_out})
+    if (p) cudaFree(p);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   delete static_cast<HostState*>(ctx->host);
   delete ctx;
@@ -582,6 +659,20 @@ int ntcb_get_tuning(ntcb_context* ctx, ntcb_tuning* t) {
   need_ctx(ctx);
   if (!t) fail(NTCB_EINVAL, "tuning: null");
   *t = ctx->tune;
+  API_CATCH
+}
+
+int ntcb_host_alloc(uint64_t bytes, void** out) {
+  API_TRY
+  if (!out) fail(NTCB_EINVAL, "host_alloc: null out");
+  *out = nullptr;
+  NTCB_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+  API_CATCH
+}
+
+int ntcb_host_free(void* p) {
+  API_TRY
+  if (p) NTCB_CUDA(cudaFreeHost(p));
   API_CATCH
 }
 
@@ -947,6 +1038,39 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
   if (!a_init && !hs.verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   if (hs.queued) collect(ctx, nullptr);  // drain (and report) anything queued before
   int pre = -1;
+  const uint64_t rows = ctx->dims[mode], R = ctx->rank, ld = ctx->ld;
+  const bool dev_io = a_init && pinned(a_init) && (!outs || ((!a_out || pinned(a_out)) && (!y_out || pinned(y_out))));
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((rows * ld + 255) / 256, 8ull * ctx->sm_count));
+  if (dev_io) {
+    // page-locked caller buffers: a_init goes to the device as fp64 and is
+    // checked and converted there; no host work on the critical path
+    if (cfg->max_inner > 0) pre = enqueue_sample(ctx, mode, 0, rows, *cfg, rng_state, 0);
+    HostState& h = hs;
+    double* din = io_buffer<double>(h.io_in, h.io_in_cap, rows * R);
+    float* dsc = io_buffer<float>(h.io_f, h.io_f_cap, rows * ld);
+    NTCB_CUDA(cudaMemcpyAsync(din, a_init, sizeof(double) * rows * R, cudaMemcpyHostToDevice, ctx->stream));
+    k_a_init_in<<<g, 256, 0, ctx->stream>>>(din, rows, static_cast<int>(R), static_cast<int>(ld), dsc, ctx->counters,
+                                           mode);
+    k_a_init_commit<<<g, 256, 0, ctx->stream>>>(dsc, rows * ld, ctx->A[mode], ctx->Y[mode], ctx->counters);
+    NTCB_CUDA(cudaGetLastError());
+    const uint64_t own = enqueue_snmc_owned(ctx, mode, 0, rows, *cfg, rng_state, pre, true);
+    if (outs && (a_out || y_out)) {
+      double* dout = io_buffer<double>(h.io_out, h.io_out_cap, 2 * rows * R);
+      k_factors_out<<<g, 256, 0, ctx->stream>>>(ctx->A[mode], ctx->Y[mode], rows, static_cast<int>(R),
+                                               static_cast<int>(ld), a_out ? dout : nullptr,
+                                               y_out ? dout + rows * R : nullptr);
+      NTCB_CUDA(cudaGetLastError());
+      if (a_out)
+        NTCB_CUDA(cudaMemcpyAsync(a_out, dout, sizeof(double) * rows * R, cudaMemcpyDeviceToHost, ctx->stream));
+      if (y_out)
+        NTCB_CUDA(cudaMemcpyAsync(y_out, dout + rows * R, sizeof(double) * rows * R, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+    }
+    collect(ctx, nullptr);  // the one synchronisation; a_init errors surface here
+    hs.verified[mode] = true;
+    if (entries_accessed) *entries_accessed += own;
+    return NTCB_OK;
+  }
   if (a_init) {
     // the first sample does not read factors: it runs on the side stream
     // while a_init is converted and copied in

@@ -175,6 +175,42 @@ def term_cond(history: List[MetricsRecord], cfg: AoConfig) -> bool:  # ao.cpp:58
 
 
 # --------------------------------------------------------------------------
+class PinnedArray(np.ndarray):
+    """numpy array over page-locked host memory (ntcb_host_alloc), freed with
+    the array; host-buffer S_NMC calls on such arrays take the device-side
+    conversion path (no host staging)."""
+
+    def __new__(cls, shape, dtype=np.float64):
+        L = _lib.load()
+        dt = np.dtype(dtype)
+        n = int(np.prod(shape)) * dt.itemsize
+        p = C.c_void_p()
+        check(L.ntcb_host_alloc(n, C.byref(p)))
+        buf = (C.c_char * max(n, 1)).from_address(p.value)
+        obj = np.ndarray.__new__(cls, shape, dt, buffer=buf)
+        obj._ptr = p.value
+        obj._owner = True
+        return obj
+
+    def __array_finalize__(self, obj):
+        self._ptr = getattr(obj, "_ptr", None)
+        self._owner = False  # views never free
+
+    def __del__(self):
+        if getattr(self, "_owner", False) and self._ptr:
+            try:
+                _lib.load().ntcb_host_free(C.c_void_p(self._ptr))
+            except Exception:
+                pass
+            self._ptr = None
+
+
+def pinned_like(a) -> "PinnedArray":
+    out = PinnedArray(np.shape(a), np.asarray(a).dtype)
+    out[...] = a
+    return out
+
+
 class Context:
     """An ntcb_context: one device, one stream, a resident tensor + factors."""
 

@@ -277,6 +277,41 @@ def test_s_nmc_edge_cases(ntc):
     assert out[0, 0] != a_init[0, 0]
 
 
+def test_host_buffers_pinned_equals_pageable(ntc):
+    """ntcb_s_nmc_host on page-locked buffers (device-side fp64 <-> fp32
+    conversion and nonnegativity check, direct copies) returns exactly what
+    the pageable path (host conversion through staging) returns, and rejects
+    a negative a_init leaving A and Y untouched."""
+    import paper_2109_09534_b200 as P
+    dims, R = [3000, 400, 50], 12
+    ctx = P.Context(0)
+    ctx.synth(dims, 1_000_000, 4, 0.01, 17)
+    ctx.random_factors(R, 3)
+    cfg = P.NmcConfig(c=0.5)
+    a0 = ctx.get_factor(0)[0]
+    outs = {}
+    for kind in ("pageable", "pinned"):
+        ctx.random_factors(R, 3)
+        mk = (lambda x: np.array(x)) if kind == "pageable" else P.pinned_like
+        ai, ao, yo = mk(a0), mk(np.zeros_like(a0)), mk(np.zeros_like(a0))
+        n = ctx.s_nmc_host(0, ai, ao, yo, cfg, 4242)
+        outs[kind] = (n, np.array(ao), np.array(yo))
+        np.testing.assert_array_equal(ao, ctx.get_factor(0)[0])
+        np.testing.assert_array_equal(yo, ctx.get_factor(0)[1])
+    assert outs["pinned"][0] == outs["pageable"][0]
+    np.testing.assert_array_equal(outs["pinned"][1], outs["pageable"][1])
+    np.testing.assert_array_equal(outs["pinned"][2], outs["pageable"][2])
+    before = ctx.get_factor(0)
+    bad = P.pinned_like(a0)
+    bad[1234, 5] = -0.5
+    with pytest.raises(ValueError, match="a_init must be nonnegative"):
+        ctx.s_nmc_host(0, bad, P.pinned_like(np.zeros_like(a0)), P.pinned_like(np.zeros_like(a0)), cfg, 4243)
+    after = ctx.get_factor(0)
+    np.testing.assert_array_equal(before[0], after[0])
+    np.testing.assert_array_equal(before[1], after[1])
+    ctx.s_nmc(1, cfg, 99)  # the context works normally afterwards
+
+
 def test_collect_counts_survive_internal_drains(ntc):
     """ntcb_collect returns the entries of every async sweep queued since the
     last collect, even when other calls (metrics, a blocking s_nmc, sampling)

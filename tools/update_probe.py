@@ -22,6 +22,8 @@ if args.tune:
 cfgd = bench.CONFIGS[args.config]
 bench.generate(ctx, cfgd, args.config)
 ctx.random_factors(cfgd["R"], 7)
+from paper_2109_09534_b200.dist import blocksizes  # noqa: E402
+print("sampled per mode", [int(blocksizes(ctx.view_offsets(m), 0.5).sum()) for m in range(len(cfgd["dims"]))])
 for k in range(args.sweeps):
     ctx.sweep_async(k, P.NmcConfig(lambda_=1e-3, c=0.5, max_inner=1), 7)
 print("entries", ctx.collect())
