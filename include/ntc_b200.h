@@ -280,6 +280,14 @@ int ntcb_relative_error(ntcb_context* ctx, double* out);
 /* masked RMSE = sqrt(sse / |Omega|). */
 int ntcb_rmse(ntcb_context* ctx, double* out);
 
+/* ---- image demo (image.cpp:161-183) ------------------------------------ */
+/* render_model: the dense H x W x 3 evaluation of the resident factors
+ * (order 3, dims[2] == 3) into 8-bit pixels, row-major (i, j, channel),
+ * quantize = lround(clamp(v, 0, 255)); fp64 sums on the device.  pixels:
+ * host buffer of 3 * dims[0] * dims[1] bytes.  invalid_argument (same text
+ * as the reference) for any other shape. */
+int ntcb_render_model(ntcb_context* ctx, uint8_t* pixels);
+
 /* ---- synthetic data (BASELINE.json configs; not in the reference) ------ */
 /* Uniform unique cells + rank-`true_rank` U[0,1) CPD values + N(0,sigma^2)
  * noise clamped at 0, generated on the device from `seed`; writes device

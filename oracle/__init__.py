@@ -317,6 +317,7 @@ def ref_lib():
         L.ref_ao_ntc.argtypes = [C.c_void_p, C.POINTER(AoCfg), _f64p, _f64p, _f64p, C.c_int,
                                  C.POINTER(C.c_int)]
         L.ref_power_method.argtypes = [C.c_uint64, _f64p, C.c_int, C.c_double, _f64p]
+        L.ref_render_model.argtypes = [C.c_int, _u64p, C.c_uint64, C.POINTER(_f64p), C.POINTER(C.c_uint8)]
         L.ref_row_step.argtypes = [C.c_uint64, _f64p, _f64p, _f64p, C.c_double, C.c_double, _f64p,
                                    _f64p, _f64p]
         L.ref_row_terms.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _u32p, C.c_uint64, _f64p,
@@ -376,6 +377,18 @@ def ref_initial_factors(dims, rank, seed):
         res.append(out[pos: pos + int(d) * rank].reshape(int(d), rank).copy())
         pos += int(d) * rank
     return res
+
+
+def ref_render_model(factors):
+    """The reference's render_model (image.cpp:161-183): (H, W, 3) uint8."""
+    fs = [np.ascontiguousarray(f, np.float64) for f in factors]
+    dims = np.array([f.shape[0] for f in fs], np.uint64)
+    R = fs[0].shape[1]
+    H, W = int(dims[0]), int(dims[1])
+    out = np.zeros(max(3 * H * W, 1), np.uint8)
+    _ref_check(ref_lib().ref_render_model(len(fs), _ptr(dims, _u64p), R, _arr_ptrs(fs, _f64p),
+                                          out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out[: 3 * H * W].reshape(H, W, 3)
 
 
 def ref_power_method(H, iters=30, tol=1e-6):

@@ -15,6 +15,7 @@
 //   row_step             proj/core/src/nmc.cpp:174-197
 //   s_nmc                proj/core/src/nmc.cpp:199-272
 //   objective/rel_error  proj/core/src/metrics.cpp:8-37
+//   render_model         proj/core/src/image.cpp:161-183
 //   ao_ntc/sweep_stream  proj/core/src/ao.cpp:65-133
 #include <cstdint>
 #include <cstring>
@@ -26,6 +27,7 @@
 
 #include "ntc/ao.hpp"
 #include "ntc/factor_set.hpp"
+#include "ntc/image.hpp"
 #include "ntc/metrics.hpp"
 #include "ntc/mode_view.hpp"
 #include "ntc/nmc.hpp"
@@ -392,6 +394,18 @@ int ref_write_tns(void* h, const char* path) {
 }
 
 // ---- per-row operators ----------------------------------------------------
+// render_model (image.cpp:161-183) on a FactorSet built from host factors.
+int ref_render_model(int order, const std::uint64_t* dims, std::uint64_t rank, const double* const* fac,
+                     std::uint8_t* pixels) {
+  return guarded([&] {
+    std::vector<std::size_t> d(dims, dims + order);
+    ntc::FactorSet f = ntc::FactorSet::zeros(d, rank);
+    for (int m = 0; m < order; ++m) f.factors[m] = to_matrix(fac[m], d[m], rank);
+    const ntc::Image img = ntc::render_model(f);
+    std::copy(img.pixels.begin(), img.pixels.end(), pixels);
+  });
+}
+
 int ref_power_method(std::uint64_t n, const double* hm, int iters, double tol, double* out) {
   return guarded([&] { *out = ntc::power_method(to_matrix(hm, n, n), iters, tol); });
 }

@@ -137,6 +137,7 @@ SIGNATURES = {
                                      C.c_uint64]),
     "ntcb_synth": (C.c_int, [C.c_void_p, C.c_int, u64p, C.c_uint64, C.c_uint64, C.c_double,
                              C.c_uint64, f64p, C.c_int]),
+    "ntcb_render_model": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     "ntcb_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "ntcb_profile_read": (C.c_int, [C.c_void_p, f64p, f64p, u64p, u64p]),
 }

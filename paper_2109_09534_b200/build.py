@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libntcb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["capi.cu", "tensor.cu", "sampler.cu", "update.cu", "metrics.cu", "synth.cu", "tns.cpp"]
+SOURCES = ["capi.cu", "tensor.cu", "sampler.cu", "update.cu", "metrics.cu", "synth.cu", "render.cu", "tns.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

@@ -40,6 +40,7 @@ void load_tensor_f64(ntcb_context* ctx, int order, const uint64_t* dims, uint64_
 void load_tensor_f32(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                      const uint32_t* idx, const float* vals, bool on_device);
 void device_metrics(ntcb_context* ctx, double* sse, double* sumsq, double* reg);
+void render_model(ntcb_context* ctx, uint8_t* d_pixels);
 void synth_uniform(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
                    uint64_t true_rank, double sigma, uint64_t seed);
 void synth_general(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
@@ -1377,6 +1378,27 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
   if (n_history) *n_history = hist.size();
   if (history)
     for (uint64_t i = 0; i < hist.size() && i < max_history; ++i) history[i] = hist[i];
+  API_CATCH
+}
+
+int ntcb_render_model(ntcb_context* ctx, uint8_t* pixels) {
+  API_TRY
+  need_ctx(ctx);
+  need_factors(ctx);
+  if (ctx->order != 3 || ctx->dims[2] != 3)
+    fail(NTCB_EINVAL, "render_model: expects an H x W x 3 factorization");  // image.cpp:162-163
+  if (!pixels) fail(NTCB_EINVAL, "render_model: null pixels");
+  collect(ctx, nullptr);
+  const uint64_t n = 3 * ctx->dims[0] * ctx->dims[1];
+  uint8_t* d = nullptr;
+  NTCB_CUDA(cudaMalloc(&d, n ? n : 1));
+  struct Free {
+    uint8_t* p;
+    ~Free() { cudaFree(p); }
+  } fr{d};
+  render_model(ctx, d);
+  NTCB_CUDA(cudaMemcpyAsync(pixels, d, n, cudaMemcpyDeviceToHost, ctx->stream));
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
   API_CATCH
 }
 

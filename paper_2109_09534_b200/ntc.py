@@ -490,6 +490,15 @@ class Context:
         return [MetricsRecord(h.epoch, h.objective, h.rel_error, h.wall_seconds, h.entries_accessed)
                 for h in hist[: min(n.value, max_history)]]
 
+    def render_model(self) -> np.ndarray:
+        """render_model (image.cpp:161-183): (H, W, 3) uint8 pixels of the
+        resident factors of an H x W x 3 tensor."""
+        order, dims, _ = self.info()
+        H, W = (dims[0], dims[1]) if order >= 2 else (0, 0)
+        out = np.zeros(max(3 * H * W, 1), np.uint8)
+        check(self.L.ntcb_render_model(self.h, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out[: 3 * H * W].reshape(H, W, 3)
+
     def profile(self, on=True):
         check(self.L.ntcb_profile_enable(self.h, int(on)))
 

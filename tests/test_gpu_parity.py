@@ -1014,3 +1014,33 @@ def test_cfg5_every_mode_vs_oracle_row_chunks(ntc, orc):
     finally:
         ctx.close()
         gc.collect()
+
+
+def test_render_model_matches_reference(ntc):
+    """render_model (image.cpp:161-183, the image demo's dense CPD
+    evaluation) on the device equals the reference's pixels bit for bit on
+    fp32-representable factors -- values below 0 / above 255 clamped, .5
+    cases rounded away from zero -- and rejects non H x W x 3 factor sets
+    with the reference's message."""
+    import paper_2109_09534_b200 as P
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(8)
+    H, W, R = 97, 81, 7
+    idx = np.array([[i, j, c] for i in range(0, H, 7) for j in range(0, W, 5) for c in range(3)], np.uint32)
+    ctx = P.Context(0)
+    ctx.load([H, W, 3], idx, np.ones(len(idx)))
+    F = [(rng.random((d, R)) * s).astype(np.float32).astype(np.float64) for d, s in ((H, 9.0), (W, 7.0), (3, 1.5))]
+    F[0][3, :] = 0.0      # black row
+    F[1][4, :] *= 40.0    # saturated column (clamped at 255)
+    ctx.set_factors(R, F)
+    got = ctx.render_model()
+    want = O.ref_render_model(F)
+    assert got.shape == (H, W, 3)
+    np.testing.assert_array_equal(got, want)
+    assert got.max() == 255 and got.min() == 0
+    c4 = P.Context(0)
+    c4.load([4, 5, 2], np.array([[0, 0, 0]], np.uint32), np.ones(1))
+    c4.random_factors(2, 1)
+    with pytest.raises(ValueError, match="render_model: expects an H x W x 3 factorization"):
+        c4.render_model()
