@@ -117,6 +117,9 @@ typedef struct ntcb_tuning {
   int32_t heavy_win_log2;    /* log2 of the heavy sampler's draw window (24) */
   int32_t heavy_big_log2;    /* log2 of the slice length taking the windowed path (24) */
   int32_t host_threads;      /* host threads for fp64 <-> fp32 factor conversion, 0 = min(cores, 16) */
+  int32_t update_carveout;   /* shared-memory carve-out preference (percent) of the update kernels,
+                                -1 = driver default; a smaller carve-out leaves more L1 for the
+                                in-flight factor-row gathers at the cost of resident CTAs */
   int32_t nat_pad;           /* ranks 9-24, orders 3-4: 128-byte factor rows + the natural-layout (NAT)
                                 update; 1 on, 0 off, -1 (default) when the factors exceed 16 MB
                                 (gathers mostly miss L1: configs 3 and 5 measured 2.6 % / 5 % faster,

@@ -1447,6 +1447,8 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
   smem = warp_bytes * wpc;
   NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 ctx->tune.update_carveout));
   int per_sm = 0;
   NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT, SHORT>, wpc * 32, smem));
   if (per_sm < 1) per_sm = 1;
