@@ -674,6 +674,7 @@ void drop_sample_plans(ntcb_context* ctx) {
 struct HeavyRow {
   uint64_t row, beg;
   uint32_t n, b;
+  uint64_t tb;  // word offset of the slice's bitmaps in the plan's bit buffer: tb[ceil(b/32)], then rb
 };
 
 __global__ void k_heavy_zero(const HeavyRow* rows, uint32_t* scratch, int* flags) {
@@ -683,10 +684,14 @@ __global__ void k_heavy_zero(const HeavyRow* rows, uint32_t* scratch, int* flags
     scratch[h.beg + t] = 0u;
 }
 
+// Draw phase.  Besides T, a head position r < b that a draw targets gets its
+// bit in the slice's L2-resident bitmap tb (T[r] != 0), which the tail
+// phase consults before touching the table.
 __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags, uint64_t root,
-                             int direct) {
+                             int direct, uint32_t* bits) {
   const HeavyRow h = rows[blockIdx.y];
   const uint64_t state = direct ? root : fork64(root, h.row);
+  uint32_t* tb = bits + h.tb;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < h.b; j += gridDim.x * blockDim.x) {
     const uint32_t bound = h.n - j;
     const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
@@ -694,7 +699,10 @@ __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags
     const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
     if (static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound) flags[blockIdx.y] = 1;
     const uint32_t r = j + static_cast<uint32_t>(u >> 32);
-    if (r != j) atomicMax(&scratch[h.beg + r], j + 1);
+    if (r != j) {
+      atomicMax(&scratch[h.beg + r], j + 1);
+      if (r < h.b) atomicOr(&tb[r >> 5], 1u << (r & 31u));
+    }
   }
 }
 
@@ -854,8 +862,8 @@ __global__ void k_heavy_head_big(const HeavyRow* rows, const int* flags, uint32_
   }
 }
 
-__global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int* flags,
-                             uint32_t* mask) {
+__global__ void k_heavy_tail(const HeavyRow* rows, const uint32_t* scratch, const int* flags,
+                             uint32_t* mask, uint32_t* bits) {
   const HeavyRow h = rows[blockIdx.y];
   if (flags[blockIdx.y]) return;
   const uint64_t gb0 = h.beg + h.b, gb1 = h.beg + h.n;
@@ -864,6 +872,8 @@ __global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int*
   const uint64_t w0 = gb0 >> 5, w1 = (gb1 - 1) >> 5;
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint32_t* sc = scratch + h.beg;
+  const uint32_t* tb = bits + h.tb;
+  uint32_t* rb = bits + h.tb + (static_cast<uint64_t>(h.b) + 31) / 32;
   for (uint64_t wb = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); wb <= w1;
        wb += kTailIlp * nwarps) {
     uint32_t v[kTailIlp];
@@ -876,48 +886,56 @@ __global__ void k_heavy_tail(const HeavyRow* rows, uint32_t* scratch, const int*
       const uint32_t tv = valid ? (scratch[g] & 0x7fffffffu) : 0u;
       walk[i] = tv != 0u;
       v[i] = tv - 1;
-      const uint32_t bits = __ballot_sync(kFull, walk[i]);
+      const uint32_t bits32 = __ballot_sync(kFull, walk[i]);
       if (lane == 0 && w <= w1) {
         if ((w << 5) >= gb0 && (w << 5) + 32 <= gb1)
-          mask[w] = bits;
-        else if (bits)
-          atomicOr(&mask[w], bits);
+          mask[w] = bits32;
+        else if (bits32)
+          atomicOr(&mask[w], bits32);
       }
     }
-    // chains: v -> T[v] - 1 until T[v] == 0 (the unpicked root)
+    // chains: v -> T[v] - 1 while T[v] != 0 (tb bit set; ~3/4 of the chains
+    // end at their first node and never read the DRAM-resident table); the
+    // unpicked root goes to the bitmap rb (chains are disjoint: one writer)
     bool any = true;
     while (any) {
+      bool cont[kTailIlp];
+#pragma unroll
+      for (int i = 0; i < kTailIlp; ++i) cont[i] = walk[i] && ((tb[v[i] >> 5] >> (v[i] & 31u)) & 1u);
       uint32_t nx[kTailIlp];
 #pragma unroll
-      for (int i = 0; i < kTailIlp; ++i) nx[i] = walk[i] ? (sc[v[i]] & 0x7fffffffu) : 0u;
+      for (int i = 0; i < kTailIlp; ++i) nx[i] = cont[i] ? (sc[v[i]] & 0x7fffffffu) : 0u;
       any = false;
 #pragma unroll
       for (int i = 0; i < kTailIlp; ++i) {
-        if (walk[i]) {
-          if (nx[i] != 0u) {
-            v[i] = nx[i] - 1;
-            any = true;
-          } else {
-            scratch[h.beg + v[i]] = 0x80000000u;  // unpicked root
-            walk[i] = false;
-          }
+        if (!walk[i]) continue;
+        if (cont[i]) {
+          v[i] = nx[i] - 1;
+          any = true;
+        } else {
+          atomicOr(&rb[v[i] >> 5], 1u << (v[i] & 31u));
+          walk[i] = false;
         }
       }
     }
   }
 }
 
-__global__ void k_heavy_head(const HeavyRow* rows, const uint32_t* scratch, const int* flags,
-                             uint32_t* mask) {
+__global__ void k_heavy_head(const HeavyRow* rows, const int* flags, uint32_t* mask, const uint32_t* bits) {
   const HeavyRow h = rows[blockIdx.y];
   if (flags[blockIdx.y] || h.b == 0) return;
+  const uint32_t* rb = bits + h.tb + (static_cast<uint64_t>(h.b) + 31) / 32;
   const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
   const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
     const uint64_t g = (w << 5) + lane;
-    const bool pick = g >= ga0 && g < ga1 && !(scratch[g] & 0x80000000u);
+    bool pick = false;
+    if (g >= ga0 && g < ga1) {
+      const uint64_t v = g - h.beg;
+      pick = !((rb[v >> 5] >> (v & 31u)) & 1u);  // picked unless an unpicked root
+    }
     const uint32_t bits = __ballot_sync(kFull, pick);
     if (lane == 0) {
       if ((w << 5) >= ga0 && (w << 5) + 32 <= ga1)
@@ -981,7 +999,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       const uint64_t n = v.h_off[p + 1] - v.h_off[p];
       const uint64_t b = blocksize_for(c, n);
       if (n > cap && b > 0) {
-        hr.push_back({p, v.h_off[p], static_cast<uint32_t>(n), static_cast<uint32_t>(b)});
+        hr.push_back({p, v.h_off[p], static_cast<uint32_t>(n), static_cast<uint32_t>(b), 0});
         maxn = std::max<uint32_t>(maxn, static_cast<uint32_t>(n));
       }
     }
@@ -1006,9 +1024,14 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
         pl.giant.push_back(h);
       }
     }
-    for (const HeavyRow& h : pl.giant) {
-      pl.bit_off.push_back(pl.bit_words);
+    // every slice: head bitmaps tb (T != 0) and rb (unpicked roots), b bits each
+    for (HeavyRow& h : hr) {
+      h.tb = pl.bit_words;
       pl.bit_words += 2 * ((static_cast<uint64_t>(h.b) + 31) / 32);
+    }
+    for (size_t i = 0; i < pl.giant.size(); ++i) {
+      pl.giant[i].tb = hr[pl.n_reg + i].tb;
+      pl.bit_off.push_back(pl.giant[i].tb);
     }
     if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * pl.bit_words));
     if (!pl.giant.empty()) {
@@ -1051,6 +1074,8 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   };
   const dim3 gz(gx(maxn), nh);
   k_heavy_zero<<<gz, 256, 0, stream>>>(d, view_scratch(ctx, mode), ctx->heavy_flags);
+  if (it->second.bit_words)
+    NTCB_CUDA(cudaMemsetAsync(it->second.bits, 0, sizeof(uint32_t) * it->second.bit_words, stream));
   const uint32_t n_reg = it->second.n_reg;
   int launches = 2;  // zero, exact
   const HeavyPlan& hp = it->second;
@@ -1068,10 +1093,10 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
     k_heavy_draw<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
-                                                                          ctx->heavy_flags + c.r0, root, direct);
+                                                                          ctx->heavy_flags + c.r0, root, direct,
+                                                                          hp.bits);
     ++launches;
   }
-  if (hp.bit_words) NTCB_CUDA(cudaMemsetAsync(hp.bits, 0, sizeof(uint32_t) * hp.bit_words, stream));
   for (size_t i = 0; i < hp.giant.size(); ++i) {
     const HeavyRow& h = hp.giant[i];
     const int wlog = ctx->tune.heavy_win_log2;
@@ -1095,9 +1120,9 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
     k_heavy_tail<<<dim3(gxc(c, (c.mx + 1) / 2 / kTailIlp), c.cnt), 256, 0, stream>>>(
-        d + c.r0, view_scratch(ctx, mode), ctx->heavy_flags + c.r0, mask);
-    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
-                                                                          ctx->heavy_flags + c.r0, mask);
+        d + c.r0, view_scratch(ctx, mode), ctx->heavy_flags + c.r0, mask, hp.bits);
+    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->heavy_flags + c.r0, mask,
+                                                                          hp.bits);
     launches += 2;
   }
   for (size_t i = 0; i < hp.giant.size(); ++i) {  // one slice per launch: its bitmaps stay in L2
