@@ -14,8 +14,9 @@ for r in rows:
         d = dict(zip(hdr, r))
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = d["Kernel Name"].split("(")[0]
-        name = name.replace("void ", "").split("<")[0] + ("<...>" if "<" in name else "")
+        name = d["Kernel Name"].replace("void ", "").replace("(anonymous namespace)::", "")
+        base = name.split("(")[0].split("<")[0]
+        name = base.split("::")[-1] + ("<...>" if "<" in name.split("(")[0] else "")
         v = float(d["Metric Value"].replace(",", ""))
         v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(d["Metric Unit"], 1e-6)
         agg[name][0] += 1
