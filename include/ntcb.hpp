@@ -179,6 +179,21 @@ class Solver {
     check(ntcb_relative_error(ctx_, &out));
     return out;
   }
+  // render_model (image.cpp:161-183): H x W x 3 pixels, row-major
+  std::vector<std::uint8_t> render_model() const {
+    std::vector<std::uint8_t> px(3 * (dims_.size() >= 2 ? dims_[0] * dims_[1] : 0));
+    check(ntcb_render_model(ctx_, px.data()));
+    return px;
+  }
+  // slab storage for a row shard (multi-GPU): only rows [r0, r1) of view `mode` stay resident
+  void keep_rows(int mode, std::uint64_t r0, std::uint64_t r1) { check(ntcb_view_keep_rows(ctx_, mode, r0, r1)); }
+  // launch policy (never changes results)
+  ntcb_tuning tuning() const {
+    ntcb_tuning t;
+    check(ntcb_get_tuning(ctx_, &t));
+    return t;
+  }
+  void set_tuning(const ntcb_tuning& t) { check(ntcb_set_tuning(ctx_, &t)); }
   ntcb_context* handle() const { return ctx_; }
 
  private:

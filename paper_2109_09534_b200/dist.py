@@ -149,7 +149,6 @@ class ShardedSweep:
 
     def __init__(self, ctx, cfg, rank: int, world: int, group=None, exchange: str = "auto",
                  slab: bool = True):
-        import os
 
         import torch
         import torch.distributed as tdist
@@ -168,8 +167,8 @@ class ShardedSweep:
             torch.cuda.set_stream(st)
         ctx.set_stream(st.cuda_stream)
         dist_on = tdist.is_available() and tdist.is_initialized()
-        if exchange == "auto":
-            exchange = os.environ.get("NTCB_EXCHANGE", "p2p")
+        if exchange == "auto":  # fused peer stores wherever every rank can map every other
+            exchange = "p2p"
         self.p2p = bool(dist_on and world > 1 and exchange == "p2p" and setup_p2p(ctx, rank, world, group))
         self.exchange = "p2p" if self.p2p else "gather"
         # the exchange runs whenever a process group exists (at world size 1 too:

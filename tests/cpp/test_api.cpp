@@ -68,6 +68,18 @@ int main() {
   EXPECT(threw);
   const double rel = ao.relative_error();
   EXPECT(std::isfinite(rel) && rel > 0.0);
+  threw = false;
+  try {
+    (void)ao.render_model();  // 6 x 5 x 4 tensor: not an H x W x 3 factorization
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()) == "render_model: expects an H x W x 3 factorization";
+  }
+  EXPECT(threw);
+  ntcb_tuning tn = ao.tuning();
+  EXPECT(tn.update_wpc == 4 && tn.nat_pad == -1);
+  tn.update_wpc = 2;
+  ao.set_tuning(tn);
+  EXPECT(ao.tuning().update_wpc == 2);
   std::printf("%s (%d failures)\n", fails ? "FAILED" : "ok", fails);
   return fails ? 1 : 0;
 }
