@@ -680,8 +680,45 @@ struct HeavyRow {
 __global__ void k_heavy_zero(const HeavyRow* rows, uint32_t* scratch, int* flags) {
   const HeavyRow h = rows[blockIdx.y];
   if (blockIdx.x == 0 && threadIdx.x == 0) flags[blockIdx.y] = 0;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < h.n; t += gridDim.x * blockDim.x)
-    scratch[h.beg + t] = 0u;
+  // 16-byte stores over the aligned body, 4-byte ones at the two ends
+  uint32_t* p = scratch + h.beg;
+  const uint32_t mis = static_cast<uint32_t>((4 - (h.beg & 3)) & 3);
+  const uint32_t head = mis < h.n ? mis : h.n;
+  const uint32_t body4 = (h.n - head) >> 2;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  if (tid < head) p[tid] = 0u;
+  uint4* q = reinterpret_cast<uint4*>(p + head);
+  for (uint32_t t = tid; t < body4; t += nth) q[t] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t tail0 = head + 4 * body4;
+  if (tid < h.n - tail0) p[tail0 + tid] = 0u;
+}
+
+// Head phase, one mask word per lane: picked = not an unpicked root, i.e.
+// the complement of the slice's rb bits (b bits; bit v = head position v)
+// aligned to the word's absolute entry positions.
+__device__ __forceinline__ void head_words(const HeavyRow& h, const uint32_t* rb, uint32_t* mask, uint64_t tid,
+                                           uint64_t nth) {
+  const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
+  const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
+  for (uint64_t w = w0 + tid; w <= w1; w += nth) {
+    const int64_t o = static_cast<int64_t>(w << 5) - static_cast<int64_t>(h.beg);  // rb bit of the word's entry 0
+    uint32_t win;
+    if (o >= 0) {
+      const uint64_t k = static_cast<uint64_t>(o) >> 5;
+      const uint32_t s = static_cast<uint32_t>(o) & 31u;
+      win = s ? (rb[k] >> s) | (rb[k + 1] << (32 - s)) : rb[k];
+    } else {
+      win = rb[0] << static_cast<uint32_t>(-o);
+    }
+    uint32_t valid = ~0u;
+    if ((w << 5) < ga0) valid &= ~0u << (ga0 - (w << 5));
+    if ((w << 5) + 32 > ga1) valid &= ~0u >> ((w << 5) + 32 - ga1);
+    const uint32_t picked = ~win & valid;
+    if (valid == ~0u)
+      mask[w] = picked;
+    else if (picked)
+      atomicOr(&mask[w], picked);
+  }
 }
 
 // Draw phase.  Besides T, a head position r < b that a draw targets gets its
@@ -841,25 +878,8 @@ __global__ void k_heavy_tail_big(const HeavyRow* rows, const uint32_t* scratch, 
 __global__ void k_heavy_head_big(const HeavyRow* rows, const int* flags, uint32_t* mask, const uint32_t* rb) {
   const HeavyRow h = rows[0];
   if (flags[0] || h.b == 0) return;
-  const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
-  const int lane = threadIdx.x & 31;
-  const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
-  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
-    const uint64_t g = (w << 5) + lane;
-    bool pick = false;
-    if (g >= ga0 && g < ga1) {
-      const uint64_t v = g - h.beg;
-      pick = !((rb[v >> 5] >> (v & 31u)) & 1u);
-    }
-    const uint32_t bits = __ballot_sync(kFull, pick);
-    if (lane == 0) {
-      if ((w << 5) >= ga0 && (w << 5) + 32 <= ga1)
-        mask[w] = bits;
-      else if (bits)
-        atomicOr(&mask[w], bits);
-    }
-  }
+  head_words(h, rb, mask, blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+             static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 __global__ void k_heavy_tail(const HeavyRow* rows, const uint32_t* scratch, const int* flags,
@@ -924,26 +944,9 @@ __global__ void k_heavy_tail(const HeavyRow* rows, const uint32_t* scratch, cons
 __global__ void k_heavy_head(const HeavyRow* rows, const int* flags, uint32_t* mask, const uint32_t* bits) {
   const HeavyRow h = rows[blockIdx.y];
   if (flags[blockIdx.y] || h.b == 0) return;
-  const uint32_t* rb = bits + h.tb + (static_cast<uint64_t>(h.b) + 31) / 32;
-  const uint64_t ga0 = h.beg, ga1 = h.beg + h.b;
-  const int lane = threadIdx.x & 31;
-  const uint64_t w0 = ga0 >> 5, w1 = (ga1 - 1) >> 5;
-  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t w = w0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w <= w1; w += nwarps) {
-    const uint64_t g = (w << 5) + lane;
-    bool pick = false;
-    if (g >= ga0 && g < ga1) {
-      const uint64_t v = g - h.beg;
-      pick = !((rb[v >> 5] >> (v & 31u)) & 1u);  // picked unless an unpicked root
-    }
-    const uint32_t bits = __ballot_sync(kFull, pick);
-    if (lane == 0) {
-      if ((w << 5) >= ga0 && (w << 5) + 32 <= ga1)
-        mask[w] = bits;
-      else if (bits)
-        atomicOr(&mask[w], bits);
-    }
-  }
+  head_words(h, bits + h.tb + (static_cast<uint64_t>(h.b) + 31) / 32, mask,
+             blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x,
+             static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // exact ordered fallback for flagged heavy slices (one warp each)
@@ -1033,7 +1036,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       pl.giant[i].tb = hr[pl.n_reg + i].tb;
       pl.bit_off.push_back(pl.giant[i].tb);
     }
-    if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * pl.bit_words));
+    if (pl.bit_words) NTCB_CUDA(cudaMalloc(&pl.bits, sizeof(uint32_t) * (pl.bit_words + 1)));  // +1: window reads
     if (!pl.giant.empty()) {
       uint64_t bmax = 0, nmax = 0;
       for (const HeavyRow& h : pl.giant) {
@@ -1072,7 +1075,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   auto gx = [&](uint64_t work) {
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ctx->sm_count * 2, (work + 256 * per - 1) / (256 * per))));
   };
-  const dim3 gz(gx(maxn), nh);
+  const dim3 gz(gx((maxn + 3) / 4), nh);  // 16-byte stores
   k_heavy_zero<<<gz, 256, 0, stream>>>(d, view_scratch(ctx, mode), ctx->heavy_flags);
   if (it->second.bit_words)
     NTCB_CUDA(cudaMemsetAsync(it->second.bits, 0, sizeof(uint32_t) * it->second.bit_words, stream));
@@ -1121,7 +1124,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     if (!c.cnt) continue;
     k_heavy_tail<<<dim3(gxc(c, (c.mx + 1) / 2 / kTailIlp), c.cnt), 256, 0, stream>>>(
         d + c.r0, view_scratch(ctx, mode), ctx->heavy_flags + c.r0, mask, hp.bits);
-    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->heavy_flags + c.r0, mask,
+    k_heavy_head<<<dim3(gxc(c, (c.mx + 1) / 2 / 32 + 1), c.cnt), 256, 0, stream>>>(d + c.r0, ctx->heavy_flags + c.r0, mask,
                                                                           hp.bits);
     launches += 2;
   }
@@ -1133,7 +1136,9 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
     uint32_t* rb = hp.bits + hp.bit_off[i] + (static_cast<uint64_t>(h.b) + 31) / 32;
     k_heavy_tail_big<<<g, 256, 0, stream>>>(d + n_reg + i, view_scratch(ctx, mode), ctx->heavy_flags + n_reg + i, mask,
                                             tb, rb);
-    k_heavy_head_big<<<g, 256, 0, stream>>>(d + n_reg + i, ctx->heavy_flags + n_reg + i, mask, rb);
+    const unsigned gh = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (h.b / 32 + 255) / 256)));
+    k_heavy_head_big<<<gh, 256, 0, stream>>>(d + n_reg + i, ctx->heavy_flags + n_reg + i, mask, rb);
     launches += 2;
   }
   k_heavy_exact<<<nh, 32, 0, stream>>>(d, view_scratch(ctx, mode), ctx->heavy_flags, mask, root, direct);
