@@ -725,10 +725,9 @@ __device__ __forceinline__ void head_words(const HeavyRow& h, const uint32_t* rb
 // bit in the slice's L2-resident bitmap tb (T[r] != 0), which the tail
 // phase consults before touching the table.
 __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags, uint64_t root,
-                             int direct, uint32_t* bits) {
+                             int direct) {
   const HeavyRow h = rows[blockIdx.y];
   const uint64_t state = direct ? root : fork64(root, h.row);
-  uint32_t* tb = bits + h.tb;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < h.b; j += gridDim.x * blockDim.x) {
     const uint32_t bound = h.n - j;
     const uint64_t x = mix64(state + static_cast<uint64_t>(j + 1) * kGolden);
@@ -736,9 +735,33 @@ __global__ void k_heavy_draw(const HeavyRow* rows, uint32_t* scratch, int* flags
     const uint64_t u = static_cast<uint64_t>(static_cast<uint32_t>(x >> 32)) * bound + (t >> 32);
     if (static_cast<uint32_t>(u) == 0u && static_cast<uint32_t>(t) < bound) flags[blockIdx.y] = 1;
     const uint32_t r = j + static_cast<uint32_t>(u >> 32);
-    if (r != j) {
-      atomicMax(&scratch[h.beg + r], j + 1);
-      if (r < h.b) atomicOr(&tb[r >> 5], 1u << (r & 31u));
+    if (r != j) atomicMax(&scratch[h.beg + r], j + 1);
+  }
+}
+
+// tb (T[v] != 0 for head positions v < b) of every heavy slice, from the
+// finished table in one streaming pass (a warp per 32 positions) -- cheaper
+// than an L2 atomicOr per head-targeting draw.
+__global__ void k_heavy_tb(const HeavyRow* rows, const uint32_t* scratch, const int* flags, uint32_t* bits) {
+  const HeavyRow h = rows[blockIdx.y];
+  if (flags[blockIdx.y] || h.b == 0) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (static_cast<uint64_t>(h.b) + 31) / 32;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  uint32_t* tb = bits + h.tb;
+  constexpr int kIlp = 8;  // words per warp step: 8 loads in flight per lane
+  for (uint64_t w0 = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w0 < nw;
+       w0 += kIlp * nwarps) {
+    uint32_t t[kIlp];
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+      const uint64_t v = ((w0 + i * nwarps) << 5) + lane;
+      t[i] = v < h.b ? scratch[h.beg + v] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+      const uint32_t word = __ballot_sync(kFull, (t[i] & 0x7fffffffu) != 0u);
+      if (lane == 0 && w0 + i * nwarps < nw) tb[w0 + i * nwarps] = word;
     }
   }
 }
@@ -831,13 +854,12 @@ __global__ void __launch_bounds__(256) k_giant_scatter(const HeavyRow* rows, uin
 // Pass 4 (one launch per window): T[r] = max(T[r], j + 1) in L2, and the
 // head-position bitmap tb (r < b: T[r] != 0).
 __global__ void k_giant_apply(const HeavyRow* rows, const uint2* pairs, const uint32_t* wbeg, int w,
-                              uint32_t* scratch, uint32_t* tb) {
+                              uint32_t* scratch) {
   const HeavyRow h = rows[0];
   const uint32_t p0 = wbeg[w], p1 = wbeg[w + 1];
   for (uint32_t i = p0 + blockIdx.x * blockDim.x + threadIdx.x; i < p1; i += gridDim.x * blockDim.x) {
     const uint2 q = pairs[i];
     atomicMax(&scratch[h.beg + q.x], q.y);
-    if (q.x < h.b) atomicOr(&tb[q.x >> 5], 1u << (q.x & 31u));
   }
 }
 
@@ -1096,8 +1118,7 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
     k_heavy_draw<<<dim3(gxc(c, (c.mx + 1) / 2), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
-                                                                          ctx->heavy_flags + c.r0, root, direct,
-                                                                          hp.bits);
+                                                                          ctx->heavy_flags + c.r0, root, direct);
     ++launches;
   }
   for (size_t i = 0; i < hp.giant.size(); ++i) {
@@ -1116,9 +1137,25 @@ int launch_sample_heavy(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, 
       const uint64_t approx = h.b / nwin + 1;  // grid sizing only
       const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
           1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (approx + 256 * per - 1) / (256 * per))));
-      k_giant_apply<<<g, 256, 0, stream>>>(dr, hp.pairs, wbeg, w, view_scratch(ctx, mode), hp.bits + hp.bit_off[i]);
+      k_giant_apply<<<g, 256, 0, stream>>>(dr, hp.pairs, wbeg, w, view_scratch(ctx, mode));
       ++launches;
     }
+  }
+  // head bitmaps tb of every heavy slice from the finished tables (grids per
+  // size class: one (chunk, slice) grid sized for the longest slice of all
+  // would launch mostly empty CTAs for the many short ones)
+  for (const Cls& c : cls) {
+    if (!c.cnt) continue;
+    k_heavy_tb<<<dim3(gxc(c, c.mx / 16 + 1), c.cnt), 256, 0, stream>>>(d + c.r0, view_scratch(ctx, mode),
+                                                                       ctx->heavy_flags + c.r0, hp.bits);
+    ++launches;
+  }
+  for (size_t i = 0; i < hp.giant.size(); ++i) {
+    const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>(static_cast<uint64_t>(ctx->sm_count) * 8, (hp.giant[i].b / 8 + 2047) / 2048)));
+    k_heavy_tb<<<dim3(g, 1), 256, 0, stream>>>(d + n_reg + i, view_scratch(ctx, mode), ctx->heavy_flags + n_reg + i,
+                                              hp.bits);
+    ++launches;
   }
   for (const Cls& c : cls) {
     if (!c.cnt) continue;
