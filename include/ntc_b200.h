@@ -120,6 +120,9 @@ typedef struct ntcb_tuning {
   int32_t update_carveout;   /* shared-memory carve-out preference (percent) of the update kernels,
                                 -1 = driver default; a smaller carve-out leaves more L1 for the
                                 in-flight factor-row gathers at the cost of resident CTAs */
+  int32_t peer_fence;        /* ordering of the rows stored into peer replicas: 1 (default) one
+                                system-scope fence per thread at kernel exit, 2 one per row,
+                                0 none (the kernel boundary + the NCCL barrier alone) */
   int32_t nat_pad;           /* ranks 9-24, orders 3-4: 128-byte factor rows + the natural-layout (NAT)
                                 update; 1 on, 0 off, -1 (default) when the factors exceed 16 MB
                                 (gathers mostly miss L1: configs 3 and 5 measured 2.6 % / 5 % faster,

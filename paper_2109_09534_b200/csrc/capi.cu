@@ -647,6 +647,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
     fail(NTCB_EINVAL, "tuning: heavy_win_log2 / heavy_big_log2 must be in [16, 30]");
   if (t->host_threads < 0) fail(NTCB_EINVAL, "tuning: host_threads must be >= 0");
   if (t->nat_pad < -1 || t->nat_pad > 1) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0 or 1");
+  if (t->peer_fence < 0 || t->peer_fence > 2) fail(NTCB_EINVAL, "tuning: peer_fence must be 0, 1 or 2");
   if (t->update_carveout < -1 || t->update_carveout > 100)
     fail(NTCB_EINVAL, "tuning: update_carveout must be -1 or a percentage");
   collect(ctx, nullptr);  // queued work keeps the plans it was launched with

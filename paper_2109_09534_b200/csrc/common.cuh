@@ -111,6 +111,7 @@ inline ntcb_tuning default_tuning() {
   t.heavy_big_log2 = 24;
   t.host_threads = 0;
   t.update_carveout = -1;
+  t.peer_fence = 1;
   t.nat_pad = -1;
   return t;
 }
