@@ -276,6 +276,36 @@ __device__ __forceinline__ void peer_fence_at_exit(const UpdateArgs& a) {
   if (a.n_peers && a.peer_fence == 1) __threadfence_system();
 }
 
+// One streamed batch (4 entries per lane: coordinates co[m], values cv,
+// sampled bits `bits`) compacted into the staging ring at `at`, in entry
+// order (warp scan of the per-lane counts).  Returns the entries added.
+// Shared by k_update and k_update_tc.
+template <int NO, int kStage>
+__device__ __forceinline__ int stage_sampled(uint32_t bits, const uint4 (&co)[NO], const uint4& cv, int no, int lane,
+                                             int at, uint32_t* st_o, float* st_x) {
+  const int c4 = __popc(bits);
+  int incl = c4;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int slot = at + incl - c4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if ((bits >> q) & 1u) {
+      const int sl = slot & (kStage - 1);
+#pragma unroll
+      for (int m = 0; m < NO; ++m)
+        if (m < no) st_o[m * kStage + sl] = q == 0 ? co[m].x : q == 1 ? co[m].y : q == 2 ? co[m].z : co[m].w;
+      st_x[sl] = __uint_as_float(q == 0 ? cv.x : q == 1 ? cv.y : q == 2 ? cv.z : cv.w);
+      ++slot;
+    }
+  }
+  return total;
+}
+
 // CUDA-core update CTA shapes: ranks <= 20 -> 8 warps x 2 CTAs (<= 128 regs);
 // 21-32 -> 4 warps x 3 CTAs (<= 170 regs, 12 warps/SM instead of 8);
 // above -> 8 warps x 1 CTA
@@ -509,27 +539,7 @@ __global__ void __launch_bounds__(k_update_threads(LD4), k_update_min_blocks(LD4
       // clip to [lo, hi)
       if (r < lo) bits &= 0xfu << (lo - r);
       if (r + 4 > hi) bits &= hi - r > 0 ? (0xfu >> (4 - (hi - r))) : 0u;
-      const int c4 = __popc(bits);
-      int incl = c4;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int slot = head + cnt + incl - c4;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((bits >> q) & 1u) {
-          const int sl = slot & (W::kStage - 1);
-#pragma unroll
-          for (int m = 0; m < NO; ++m)
-            if (m < no) st_o[m * W::kStage + sl] = q == 0 ? co[m].x : q == 1 ? co[m].y : q == 2 ? co[m].z : co[m].w;
-          st_x[sl] = __uint_as_float(q == 0 ? cv.x : q == 1 ? cv.y : q == 2 ? cv.z : cv.w);
-          ++slot;
-        }
-      }
-      cnt += total;
+      cnt += stage_sampled<NO, W::kStage>(bits, co, cv, no, lane, head + cnt, st_o, st_x);
       __syncwarp();
       drain_full();
     }
@@ -1051,27 +1061,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       uint32_t bits = full ? 0xfu : (rmsk[buf * 32 + (lane >> 3)] >> ((sh0 + static_cast<uint32_t>(r)) & 31u)) & 0xfu;
       if (r < lo) bits &= 0xfu << (lo - r);
       if (r + 4 > hi) bits &= hi - r > 0 ? (0xfu >> (4 - (hi - r))) : 0u;
-      const int c4 = __popc(bits);
-      int incl = c4;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int slot = head + cnt + incl - c4;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if ((bits >> q) & 1u) {
-          const int sl = slot & (W::kStage - 1);
-#pragma unroll
-          for (int m = 0; m < NO; ++m)
-            if (m < no) st_o[m * W::kStage + sl] = q == 0 ? co[m].x : q == 1 ? co[m].y : q == 2 ? co[m].z : co[m].w;
-          st_x[sl] = __uint_as_float(q == 0 ? cv.x : q == 1 ? cv.y : q == 2 ? cv.z : cv.w);
-          ++slot;
-        }
-      }
-      cnt += total;
+      cnt += stage_sampled<NO, W::kStage>(bits, co, cv, no, lane, head + cnt, st_o, st_x);
       __syncwarp();
       drain_full();
     }
