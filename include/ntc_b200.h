@@ -120,6 +120,8 @@ typedef struct ntcb_tuning {
   int32_t update_carveout;   /* shared-memory carve-out preference (percent) of the update kernels,
                                 -1 = driver default; a smaller carve-out leaves more L1 for the
                                 in-flight factor-row gathers at the cost of resident CTAs */
+  int32_t graph;             /* 1: ntcb_sweep_async / ntcb_ao_ntc launch each sweep as one CUDA graph
+                                (captured per sweep, updated in place), 0: stream launches */
   int32_t peer_fence;        /* ordering of the rows stored into peer replicas: 1 (default) one
                                 system-scope fence per thread at kernel exit, 2 one per row,
                                 0 none (the kernel boundary + the NCCL barrier alone) */

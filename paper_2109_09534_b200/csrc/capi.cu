@@ -61,6 +61,9 @@ struct HostState {
   std::map<std::tuple<int, uint64_t, uint64_t, uint64_t>, uint64_t> bs_cache;
   float* stage = nullptr;  // pinned fp32 staging for host-buffer factor transfers
   uint64_t stage_n = 0;    // floats
+  cudaGraphExec_t sweep_exec = nullptr;  // the sweep graph (ntcb_tuning.graph)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  uint64_t sweep_warm = 0;  // plan epoch + 1 of the last uncaptured sweep (plans and buffers exist)
   void* io_in = nullptr;   // device fp64 a_init / fp32 scratch / fp64 outputs (pinned-buffer path)
   void* io_f = nullptr;
   void* io_out = nullptr;
@@ -222,6 +225,69 @@ uint64_t enqueue_snmc_owned(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r
                             bool y_set = false) {
   const uint64_t n = enqueue_snmc(ctx, mode, r0, r1, cfg, rng_state, presampled, y_set);
   host_of(ctx).pending_accessed -= n;
+  return n;
+}
+
+// One AO iteration (every mode, Gauss-Seidel, ao.cpp:121-124) enqueued on the
+// context's streams; returns its entries.  With ntcb_tuning.graph the sweep
+// is captured into a CUDA graph (the side stream forked into the capture and
+// joined back) and launched as one unit -- the graph exec is updated in place
+// from sweep to sweep (same topology, new RNG roots and mask parities).  The
+// first sweep of a context runs uncaptured: plans and buffers are allocated
+// there, outside any capture.  Sweeps launched as graphs serialise on the
+// stream, so their waits on the previous sweep's mask events are dropped.
+uint64_t enqueue_sweep(ntcb_context* ctx, uint64_t k, const ntcb_nmc_config& cfg, uint64_t seed, bool owned) {
+  HostState& hs = host_of(ctx);
+  auto one = [&](int i) {
+    const uint64_t st = fork64(fork64(fork64(seed, 2), k), static_cast<uint64_t>(i));  // ao.cpp:65-68
+    return owned ? enqueue_snmc_owned(ctx, i, 0, ctx->dims[i], cfg, st) : enqueue_snmc(ctx, i, 0, ctx->dims[i], cfg, st);
+  };
+  uint64_t n = 0;
+  if (!ctx->tune.graph || hs.sweep_warm != ctx->plan_epoch + 1 || ctx->prof.on) {
+    for (int i = 0; i < ctx->order; ++i) n += one(i);
+    hs.sweep_warm = ctx->plan_epoch + 1;  // plans of this epoch exist now
+    return n;
+  }
+  if (!hs.ev_fork) NTCB_CUDA(cudaEventCreateWithFlags(&hs.ev_fork, cudaEventDisableTiming));
+  if (!hs.ev_join) NTCB_CUDA(cudaEventCreateWithFlags(&hs.ev_join, cudaEventDisableTiming));
+  for (auto& mm : ctx->consumed_valid) mm[0] = mm[1] = false;
+  NTCB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  cudaGraph_t g = nullptr;
+  try {
+    NTCB_CUDA(cudaEventRecord(hs.ev_fork, ctx->stream));
+    NTCB_CUDA(cudaStreamWaitEvent(ctx->side, hs.ev_fork, 0));
+    for (int i = 0; i < ctx->order; ++i) n += one(i);
+    NTCB_CUDA(cudaEventRecord(hs.ev_join, ctx->side));
+    NTCB_CUDA(cudaStreamWaitEvent(ctx->stream, hs.ev_join, 0));
+  } catch (...) {
+    cudaStreamEndCapture(ctx->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    throw;
+  }
+  NTCB_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+  if (hs.sweep_exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(hs.sweep_exec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(hs.sweep_exec);
+      hs.sweep_exec = nullptr;
+    }
+  }
+  if (!hs.sweep_exec) {
+    const cudaError_t e = cudaGraphInstantiate(&hs.sweep_exec, g, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      NTCB_CUDA(e);
+    }
+  }
+  cudaGraphDestroy(g);
+  NTCB_CUDA(cudaGraphLaunch(hs.sweep_exec, ctx->stream));
+  // later side-stream work (the next sweep's samples) starts after the graph;
+  // the mask events recorded inside the capture are not waited on again
+  NTCB_CUDA(cudaEventRecord(hs.ev_fork, ctx->stream));
+  NTCB_CUDA(cudaStreamWaitEvent(ctx->side, hs.ev_fork, 0));
+  for (auto& mm : ctx->consumed_valid) mm[0] = mm[1] = false;
   return n;
 }
 
@@ -610,6 +676,9 @@ int ntcb_destroy(ntcb_context* ctx) {
   if (host_of(ctx).stage) cudaFreeHost(host_of(ctx).stage);
   for (void* p : {host_of(ctx).io_in, host_of(ctx).io_f, host_of(ctx).io_out})
     if (p) cudaFree(p);
+  if (host_of(ctx).sweep_exec) cudaGraphExecDestroy(host_of(ctx).sweep_exec);
+  if (host_of(ctx).ev_fork) cudaEventDestroy(host_of(ctx).ev_fork);
+  if (host_of(ctx).ev_join) cudaEventDestroy(host_of(ctx).ev_join);
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   delete static_cast<HostState*>(ctx->host);
   delete ctx;
@@ -648,6 +717,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
   if (t->host_threads < 0) fail(NTCB_EINVAL, "tuning: host_threads must be >= 0");
   if (t->nat_pad < -1 || t->nat_pad > 1) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0 or 1");
   if (t->peer_fence < 0 || t->peer_fence > 2) fail(NTCB_EINVAL, "tuning: peer_fence must be 0, 1 or 2");
+  if (t->graph != 0 && t->graph != 1) fail(NTCB_EINVAL, "tuning: graph must be 0 or 1");
   if (t->update_carveout < -1 || t->update_carveout > 100)
     fail(NTCB_EINVAL, "tuning: update_carveout must be -1 or a percentage");
   collect(ctx, nullptr);  // queued work keeps the plans it was launched with
@@ -1229,10 +1299,9 @@ int ntcb_sweep_async(ntcb_context* ctx, uint64_t sweep, const ntcb_nmc_config* c
   validate_nmc(cfg);
   need_factors(ctx);
   need_whole(ctx);
-  for (int i = 0; i < ctx->order; ++i) {
+  for (int i = 0; i < ctx->order; ++i)
     if (!host_of(ctx).verified[i]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
-    enqueue_snmc(ctx, i, 0, ctx->dims[i], *cfg, ntcb_sweep_stream_state(seed, sweep, i));
-  }
+  enqueue_sweep(ctx, sweep, *cfg, seed, false);
   API_CATCH
 }
 
@@ -1363,9 +1432,7 @@ int ntcb_ao_ntc(ntcb_context* ctx, const ntcb_ao_config* cfg, ntcb_metrics_recor
   for (uint64_t k = 0;; ++k) {
     if (static_cast<double>(accessed) / static_cast<double>(ctx->nnz) >= cfg->max_epochs) break;
     if (plateau(hist, cfg->term_tol)) break;
-    uint64_t st = 0;
-    for (int i = 0; i < ctx->order; ++i)
-      st += enqueue_snmc_owned(ctx, i, 0, ctx->dims[i], n, ntcb_sweep_stream_state(cfg->seed, k, i));
+    const uint64_t st = enqueue_sweep(ctx, k, n, cfg->seed, true);
     if (st == 0) break;
     accessed += st;
     last_recorded = ((k + 1) % static_cast<uint64_t>(cfg->metrics_every) == 0);

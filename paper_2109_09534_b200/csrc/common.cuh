@@ -112,6 +112,7 @@ inline ntcb_tuning default_tuning() {
   t.host_threads = 0;
   t.update_carveout = -1;
   t.peer_fence = 1;
+  t.graph = 0;
   t.nat_pad = -1;
   return t;
 }
@@ -168,6 +169,7 @@ struct ntcb_context {
   int error_mode = -1;    // mode of the queued updates (error text)
 
   ntcb_tuning tune = ntcb::default_tuning();
+  uint64_t plan_epoch = 0;              // bumped whenever cached launch plans are dropped
   void* cache[ntcb::kCacheSlots] = {};  // per-TU plan maps (see CacheSlot)
   void* host = nullptr;                 // capi.cu host bookkeeping (HostState)
 

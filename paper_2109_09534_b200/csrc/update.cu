@@ -1389,6 +1389,7 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
 }
 
 void drop_plans(ntcb_context* ctx) {
+  ++ctx->plan_epoch;  // a captured sweep graph must be rebuilt from an uncaptured sweep
   if (!ctx->cache[kCacheUpdate]) return;
   for (auto& kv : ctx_cache<WorkPlans>(ctx, kCacheUpdate)) {
     if (kv.second.d_items) cudaFree(kv.second.d_items);

@@ -1044,3 +1044,31 @@ def test_render_model_matches_reference(ntc):
     c4.random_factors(2, 1)
     with pytest.raises(ValueError, match="render_model: expects an H x W x 3 factorization"):
         c4.render_model()
+
+
+def test_sweep_graph_equals_stream_launches(ntc):
+    """ntcb_tuning.graph: sweeps launched as CUDA graphs (captured per sweep,
+    updated in place) give bitwise the factors and counts of stream-launched
+    sweeps, through ntcb_sweep_async and ntcb_ao_ntc, with heavy slices (the
+    grid sampler's launches) in the graph."""
+    import paper_2109_09534_b200 as P
+    dims, R = [2000, 300, 40], 8
+    out = {}
+    for graph in (0, 1):
+        ctx = P.Context(0)
+        ctx.set_tuning(graph=graph)
+        ctx.synth(dims, 3_000_000, 4, 0.01, 5, [1.1, 0.0, 0.0], 0)
+        ctx.random_factors(R, 7)
+        for k in range(5):
+            ctx.sweep_async(k, P.NmcConfig(c=0.5), 7)
+        ctx.profile(True)  # stream launches in between (profiling disables capture)
+        ctx.sweep_async(5, P.NmcConfig(c=0.5), 7)
+        ctx.profile(False)
+        ctx.sweep_async(6, P.NmcConfig(c=0.5), 7)
+        n = ctx.collect()
+        hist = ctx.ao_ntc(P.AoConfig(rank=R, c=0.5, max_epochs=4.0, seed=3, eval_metrics=False))
+        out[graph] = (n, [h.entries_accessed for h in hist], [ctx.get_factor(m) for m in range(3)])
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    for m in range(3):
+        np.testing.assert_array_equal(out[0][2][m][0], out[1][2][m][0])
+        np.testing.assert_array_equal(out[0][2][m][1], out[1][2][m][1])
