@@ -244,6 +244,21 @@ int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a
  * Asynchronous: errors and the count are collected by ntcb_collect(). */
 int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
                           const ntcb_nmc_config* cfg, uint64_t rng_state);
+/* Heavy rows shared by several ranks (max_inner = 1).  A row of a mode is cut
+ * into ntcb_segment_length()-entry chunks from its start (a property of the
+ * mode: any partition cuts it the same way).  ntcb_s_nmc_chunks_async samples
+ * the row (its stream RngStream(rng_state).fork(0).fork(row)) and writes the
+ * fp32 (H, w) partials of chunks [chunk_begin, chunk_end) -- R*R + R floats
+ * each, in chunk order -- to the device buffer d_slots, finalising nothing;
+ * ntcb_finalize_row_async takes the row's complete set (every chunk, in
+ * order, gathered from the ranks) and sums, steps and stores the row exactly
+ * as a single-GPU call does (bitwise), counting its entries once. */
+int ntcb_segment_length(ntcb_context* ctx, int mode, uint64_t* seg);
+int ntcb_s_nmc_chunks_async(ntcb_context* ctx, int mode, uint64_t row, uint32_t chunk_begin,
+                            uint32_t chunk_end, const ntcb_nmc_config* cfg, uint64_t rng_state,
+                            void* d_slots);
+int ntcb_finalize_row_async(ntcb_context* ctx, int mode, uint64_t row, const void* d_slots,
+                            uint32_t nslots, const ntcb_nmc_config* cfg);
 /* Waits for queued work; adds the entries accessed since the last collect
  * to *entries_accessed and reports the first row failure (lowest row). */
 int ntcb_collect(ntcb_context* ctx, uint64_t* entries_accessed);

@@ -121,6 +121,11 @@ SIGNATURES = {
     "ntcb_s_nmc_rows_async": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64,
                                         C.POINTER(NmcConfigC), C.c_uint64]),
     "ntcb_collect": (C.c_int, [C.c_void_p, u64p]),
+    "ntcb_segment_length": (C.c_int, [C.c_void_p, C.c_int, u64p]),
+    "ntcb_s_nmc_chunks_async": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32,
+                                          C.POINTER(NmcConfigC), C.c_uint64, C.c_void_p]),
+    "ntcb_finalize_row_async": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p, C.c_uint32,
+                                          C.POINTER(NmcConfigC)]),
     "ntcb_sample_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
                                    C.c_uint64, C.c_uint64, u64p, u32p]),
     "ntcb_sample_mask": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_uint64,

@@ -24,6 +24,11 @@ int launch_sample(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mo
                   uint32_t* dbg_picks, const uint64_t* dbg_off, int direct = 0);
 int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
                   const ntcb_nmc_config& cfg, const uint32_t* mask);
+int launch_update_chunks(ntcb_context* ctx, int mode, uint64_t row, uint32_t cb, uint32_t ce,
+                         const ntcb_nmc_config& cfg, const uint32_t* mask, float* slots_out);
+int launch_finalize_row(ntcb_context* ctx, int mode, uint64_t row, const float* slots, uint32_t nslots,
+                        const ntcb_nmc_config& cfg);
+uint64_t segment_length(const ntcb_context* ctx, int mode);
 int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, int mode,
                       uint64_t row_begin, uint64_t row_end, double c, uint64_t root, int direct,
                       uint64_t* heavy_cap);
@@ -1187,6 +1192,59 @@ int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint6
   need_rows(ctx, mode, row_begin, row_end);
   if (!host_of(ctx).verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
   enqueue_snmc(ctx, mode, row_begin, row_end, *cfg, rng_state);
+  API_CATCH
+}
+
+int ntcb_segment_length(ntcb_context* ctx, int mode, uint64_t* seg) {
+  API_TRY
+  need_ctx(ctx);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_ERANGE, "segment_length: mode out of range");
+  if (seg) *seg = segment_length(ctx, mode);
+  API_CATCH
+}
+
+int ntcb_s_nmc_chunks_async(ntcb_context* ctx, int mode, uint64_t row, uint32_t chunk_begin,
+                            uint32_t chunk_end, const ntcb_nmc_config* cfg, uint64_t rng_state, void* d_slots) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  if (row >= ctx->dims[mode]) fail(NTCB_ERANGE, "s_nmc_chunks: row out of range");
+  need_rows(ctx, mode, row, row + 1);
+  if (cfg->max_inner != 1) fail(NTCB_EINVAL, "s_nmc_chunks: a shared row needs max_inner = 1");
+  if (!d_slots) fail(NTCB_EINVAL, "s_nmc_chunks: null slot buffer");
+  if (!host_of(ctx).verified[mode]) fail(NTCB_EINVAL, "s_nmc: a_init must be nonnegative");
+  const int par = enqueue_sample(ctx, mode, row, row + 1, *cfg, rng_state, 0);
+  const DeviceView& v = ctx->views[mode];
+  if (cfg->c < 1.0 && v.h_off[row + 1] > v.h_off[row])
+    NTCB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_sampled[mode][par], 0));
+  ctx->prof.launches += launch_update_chunks(ctx, mode, row, chunk_begin, chunk_end, *cfg, ctx->mask[mode][par],
+                                             static_cast<float*>(d_slots));
+  NTCB_CUDA(cudaEventRecord(ctx->ev_consumed[mode][par], ctx->stream));
+  ctx->consumed_valid[mode][par] = true;
+  host_of(ctx).queued = true;
+  API_CATCH
+}
+
+int ntcb_finalize_row_async(ntcb_context* ctx, int mode, uint64_t row, const void* d_slots, uint32_t nslots,
+                            const ntcb_nmc_config* cfg) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_factors(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  if (row >= ctx->dims[mode]) fail(NTCB_ERANGE, "finalize_row: row out of range");
+  if (cfg->max_inner != 1) fail(NTCB_EINVAL, "s_nmc_chunks: a shared row needs max_inner = 1");
+  if (!d_slots) fail(NTCB_EINVAL, "finalize_row: null slot buffer");
+  const uint64_t n = ctx->views[mode].h_off[row + 1] - ctx->views[mode].h_off[row];
+  const uint64_t seg = segment_length(ctx, mode);
+  if (nslots != (n + seg - 1) / seg) fail(NTCB_EINVAL, "finalize_row: slot count differs from the row's chunks");
+  const uint64_t b = blocksize_for(cfg->c, n);
+  if (b > 0) ctx->prof.launches += launch_finalize_row(ctx, mode, row, static_cast<const float*>(d_slots), nslots, *cfg);
+  host_of(ctx).pending_accessed += b;  // nmc.cpp:238, counted once (by the row's owner)
+  host_of(ctx).queued = true;
   API_CATCH
 }
 

@@ -1473,6 +1473,47 @@ static int launch_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_
   return launch_items_tc<P, 3>(ctx, a, pl, smem);
 }
 
+// The finalisation launches of a plan: rows split into <= kFinSmall slots (a
+// warp each), then slot groups and a CTA per row for the longer ones.
+template <int LD4>
+static int launch_finalize_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
+  using W = WarpSmem<LD4>;
+  const size_t smem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 * kWarps;
+  int launches = 0;
+  if (pl.n_small) {  // warp per row
+    NTCB_CUDA(cudaFuncSetAttribute(k_finalize_small<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    UpdateArgs b = a;
+    b.fins = pl.d_fins;
+    b.n_fins = pl.n_small;
+    const uint64_t fg = std::min<uint64_t>((pl.n_small + kWarps - 1) / kWarps,
+                                           static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_finalize_small<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(b);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (pl.n_groups) {  // big rows, level 1: slot groups over the whole grid
+    const uint64_t gg = std::min<uint64_t>((pl.n_groups + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_slot_groups<<<static_cast<unsigned>(gg), kWarps * 32, 0, ctx->stream>>>(a);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  if (pl.n_fins > pl.n_small) {  // CTA per row
+    // warp 0's row-end layout + the per-warp partial sums of one pass
+    const size_t fsmem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
+    NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(fsmem)));
+    UpdateArgs b = a;
+    b.fins = pl.d_fins + pl.n_small;
+    b.n_fins = pl.n_fins - pl.n_small;
+    const uint64_t fg = std::min<uint64_t>(b.n_fins, static_cast<uint64_t>(ctx->sm_count) * 4);
+    k_finalize<LD4><<<static_cast<unsigned>(fg), kWarps * 32, fsmem, ctx->stream>>>(b);
+    NTCB_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
+}
+
 template <int LD4>
 static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   using W = WarpSmem<LD4>;
@@ -1527,48 +1568,140 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
     else
       launches += launch_items<LD4, NTCB_MAX_ORDER - 1>(ctx, a, pl, smem);
   }
-  if (pl.n_small) {  // warp per row
-    NTCB_CUDA(cudaFuncSetAttribute(k_finalize_small<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    UpdateArgs b = a;
-    b.fins = pl.d_fins;
-    b.n_fins = pl.n_small;
-    const uint64_t fg = std::min<uint64_t>((pl.n_small + kWarps - 1) / kWarps,
-                                           static_cast<uint64_t>(ctx->sm_count) * 4);
-    k_finalize_small<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(b);
-    NTCB_CUDA(cudaGetLastError());
-    ++launches;
-  }
-  if (pl.n_groups) {  // big rows, level 1: slot groups over the whole grid
-    const uint64_t gg = std::min<uint64_t>((pl.n_groups + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * 4);
-    k_slot_groups<<<static_cast<unsigned>(gg), kWarps * 32, 0, ctx->stream>>>(a);
-    NTCB_CUDA(cudaGetLastError());
-    ++launches;
-  }
-  if (pl.n_fins > pl.n_small) {  // CTA per row
-    // warp 0's row-end layout + the per-warp partial sums of one pass
-    const size_t fsmem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
-    NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(fsmem)));
-    UpdateArgs b = a;
-    b.fins = pl.d_fins + pl.n_small;
-    b.n_fins = pl.n_fins - pl.n_small;
-    const uint64_t fg = std::min<uint64_t>(b.n_fins, static_cast<uint64_t>(ctx->sm_count) * 4);
-    k_finalize<LD4><<<static_cast<unsigned>(fg), kWarps * 32, fsmem, ctx->stream>>>(b);
-    NTCB_CUDA(cudaGetLastError());
-    ++launches;
-  }
+  launches += launch_finalize_ld<LD4>(ctx, a, pl);
   return launches;
 }
+
+static int launch_plan(ntcb_context* ctx, int mode, const WorkPlan& pl, const ntcb_nmc_config& cfg,
+                       const uint32_t* mask, float* slots_out);
 
 int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
                   const ntcb_nmc_config& cfg, const uint32_t* mask) {
   if (row_end <= row_begin) return 0;
-  const DeviceView& v = ctx->views[mode];
   const WorkPlan& pl = plan_for(ctx, mode, row_begin, row_end, cfg.c);
   if (pl.n_items == 0) return 0;
+  return launch_plan(ctx, mode, pl, cfg, mask, nullptr);
+}
+
+// Chunks [cb, ce) of one row -- the row's segment_length() pieces from its
+// start, exactly the items a whole-row plan cuts it into -- with their fp32
+// (H, w) partials written to slots_out[(chunk - cb) (R^2 + R)] and nothing
+// finalised: a heavy row shared by several ranks.  The same kernel
+// instantiation as the whole-mode plans, so the partials are the bits the
+// single-GPU run sums.
+int launch_update_chunks(ntcb_context* ctx, int mode, uint64_t row, uint32_t cb, uint32_t ce,
+                         const ntcb_nmc_config& cfg, const uint32_t* mask, float* slots_out) {
+  const uint64_t* off = ctx->views[mode].h_off;
+  const uint64_t seg = segment_length(ctx, mode), n = off[row + 1] - off[row];
+  const uint64_t ns = (n + seg - 1) / seg;
+  if (ce > ns || cb >= ce) fail(NTCB_ERANGE, "s_nmc_chunks: chunk range out of bounds");
+  uint64_t cbits;
+  std::memcpy(&cbits, &cfg.c, 8);
+  auto& g_plans = ctx_cache<WorkPlans>(ctx, kCacheUpdate);
+  auto key = std::make_tuple(static_cast<const void*>(ctx->views[mode].off), mode + 128, row,
+                             (static_cast<uint64_t>(cb) << 32) | ce, cbits);
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    std::vector<WorkItem> items;
+    for (uint64_t s = cb; s < ce; ++s)
+      items.push_back({row, off[row] + s * seg, std::min(off[row + 1], off[row] + (s + 1) * seg),
+                       static_cast<int64_t>(s - cb)});
+    std::stable_sort(items.begin(), items.end(), [](const WorkItem& x, const WorkItem& y) {
+      return (x.e1 - x.e0) > (y.e1 - y.e0);
+    });
+    WorkPlan pl;
+    pl.n_items = items.size();
+    pl.n_slots = ce - cb;
+    for (const WorkItem& w : items) pl.n_entries += w.e1 - w.e0;
+    NTCB_CUDA(cudaMalloc(&pl.d_items, sizeof(WorkItem) * pl.n_items));
+    NTCB_CUDA(cudaMemcpy(pl.d_items, items.data(), sizeof(WorkItem) * pl.n_items, cudaMemcpyHostToDevice));
+    it = g_plans.emplace(key, pl).first;
+  }
+  return launch_plan(ctx, mode, it->second, cfg, mask, slots_out);
+}
+
+// A shared row's complete slot set (its chunks in order, fp32) summed in the
+// canonical order -- a warp in slot order up to kFinSmall slots, slot groups
+// then group order above, as the whole-mode plans do -- and finalised (power
+// method, step, momentum, peer stores).  Y = A (a_init) for the row first.
+int launch_finalize_row(ntcb_context* ctx, int mode, uint64_t row, const float* slots, uint32_t nslots,
+                        const ntcb_nmc_config& cfg) {
+  const uint64_t R = ctx->rank, NE = R * R + R, ld = ctx->ld;
+  NTCB_CUDA(cudaMemcpyAsync(ctx->Y[mode] + row * ld, ctx->A[mode] + row * ld, sizeof(float) * ld,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  uint64_t cbits;
+  std::memcpy(&cbits, &cfg.c, 8);
+  auto& g_plans = ctx_cache<WorkPlans>(ctx, kCacheUpdate);
+  auto key = std::make_tuple(static_cast<const void*>(ctx->views[mode].off), mode + 192, row,
+                             static_cast<uint64_t>(nslots), cbits);
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    WorkPlan pl;
+    FinItem f{row, 0, static_cast<int32_t>(nslots), 0, 0};
+    std::vector<SlotGroup> groups;
+    if (nslots > static_cast<uint32_t>(kFinSmall)) {
+      f.ngroups = static_cast<int32_t>((nslots + kSlotGroup - 1) / kSlotGroup);
+      for (int32_t g = 0; g < f.ngroups; ++g)
+        groups.push_back({static_cast<int64_t>(g) * kSlotGroup, g,
+                          std::min<int32_t>(kSlotGroup, static_cast<int32_t>(nslots) - g * kSlotGroup), 0});
+    } else {
+      pl.n_small = 1;
+    }
+    pl.n_fins = 1;
+    pl.n_groups = groups.size();
+    NTCB_CUDA(cudaMalloc(&pl.d_fins, sizeof(FinItem)));
+    NTCB_CUDA(cudaMemcpy(pl.d_fins, &f, sizeof(FinItem), cudaMemcpyHostToDevice));
+    if (pl.n_groups) {
+      NTCB_CUDA(cudaMalloc(&pl.d_groups, sizeof(SlotGroup) * pl.n_groups));
+      NTCB_CUDA(cudaMemcpy(pl.d_groups, groups.data(), sizeof(SlotGroup) * pl.n_groups, cudaMemcpyHostToDevice));
+    }
+    it = g_plans.emplace(key, pl).first;
+  }
+  const WorkPlan& pl = it->second;
+  if (pl.n_groups && ctx->partial_n < 2 * pl.n_groups * NE) {  // fp64 group sums
+    if (ctx->partial) cudaFree(ctx->partial);
+    NTCB_CUDA(cudaMalloc(&ctx->partial, sizeof(float) * 2 * pl.n_groups * NE));
+    ctx->partial_n = 2 * pl.n_groups * NE;
+  }
+  UpdateArgs a{};
+  a.no = ctx->order - 1;
+  a.mode = mode;
+  a.rank = static_cast<int>(R);
+  a.ld = static_cast<int>(ld);
+  a.A = ctx->A[mode];
+  a.Y = ctx->Y[mode];
+  a.n_peers = ctx->n_peers[mode];
+  a.peer_fence = ctx->tune.peer_fence;
+  for (int q = 0; q < 7; ++q) a.peerA[q] = ctx->peerA[mode][q];
+  a.partial = const_cast<float*>(slots);
+  a.gpart = reinterpret_cast<double*>(ctx->partial);
+  a.groups = pl.d_groups;
+  a.n_groups = pl.n_groups;
+  a.fins = pl.d_fins;
+  a.n_fins = 1;
+  a.c = cfg.c;
+  a.lambda = cfg.lambda;
+  a.power_tol = cfg.power_tol;
+  a.power_iters = cfg.power_iters;
+  a.counters = ctx->counters;
+  const int LD4 = static_cast<int>(ld / 4);
+  switch (LD4) {
+#define NTCB_LD(x) \
+  case x:          \
+    return launch_finalize_ld<x>(ctx, a, pl);
+    NTCB_LD(1) NTCB_LD(2) NTCB_LD(3) NTCB_LD(4) NTCB_LD(5) NTCB_LD(6) NTCB_LD(7) NTCB_LD(8)
+    NTCB_LD(9) NTCB_LD(10) NTCB_LD(11) NTCB_LD(12) NTCB_LD(13) NTCB_LD(14) NTCB_LD(15) NTCB_LD(16)
+#undef NTCB_LD
+    default:
+      fail(NTCB_EINVAL, "s_nmc: rank exceeds the supported maximum (64)");
+  }
+}
+
+static int launch_plan(ntcb_context* ctx, int mode, const WorkPlan& pl, const ntcb_nmc_config& cfg,
+                       const uint32_t* mask, float* slots_out) {
+  const DeviceView& v = ctx->views[mode];
   const uint64_t R = ctx->rank;
-  if (pl.n_slots) {
+  if (pl.n_slots && !slots_out) {
     // slots (fp32), then the slot-group sums (fp64) of the big rows
     const uint64_t slot_words = (pl.n_slots * (R * R + R) + 1) & ~1ull;
     const uint64_t need = slot_words + 2 * pl.n_groups * (R * R + R);
@@ -1602,7 +1735,7 @@ int launch_update(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_
   a.n_items = pl.n_items;
   a.fins = pl.d_fins;
   a.n_fins = pl.n_fins;
-  a.partial = ctx->partial;
+  a.partial = slots_out ? slots_out : ctx->partial;
   a.gpart = pl.n_groups ? reinterpret_cast<double*>(ctx->partial + ((pl.n_slots * (R * R + R) + 1) & ~1ull)) : nullptr;
   a.groups = pl.d_groups;
   a.n_groups = pl.n_groups;

@@ -53,6 +53,102 @@ def partition_rows(offsets: np.ndarray, c: float, world: int) -> List[Tuple[int,
     return [(cuts[k], cuts[k + 1]) for k in range(world)]
 
 
+class Shard:
+    """One rank's part of a mode update.  full = whole rows [r0, r1); parts =
+    chunk ranges (row, cb, ce) of heavy rows shared with other ranks (chunks
+    of segment_length entries from the row start); owned = rows [o0, o1)
+    this rank finalises and publishes (its whole rows plus the shared rows
+    whose chunk 0 it holds); keep = rows [k0, k1) whose entries it needs."""
+
+    def __init__(self, full, parts, owned, keep):
+        self.full, self.parts, self.owned, self.keep = tuple(full), list(parts), tuple(owned), tuple(keep)
+
+    def __repr__(self):
+        return f"Shard(full={self.full}, parts={self.parts}, owned={self.owned}, keep={self.keep})"
+
+
+def partition_split(offsets: np.ndarray, c: float, world: int, seg: int, max_share: float = 0.5) -> List[Shard]:
+    """Contiguous ranges over work units balancing sum(n_p/2 + b_p) (+ a
+    per-row overhead), where a unit is a whole row -- or, for a row whose
+    work exceeds max_share of a rank's share, each of its chunks (seg
+    entries from the row start, the library's segment_length).  A heavy row
+    can so be split across ranks: every sharing rank computes its chunks'
+    partial sums and the owner (chunk 0) sums all of them in chunk order --
+    the association of a single-GPU run, so results stay bitwise identical."""
+    off = np.asarray(offsets, np.int64)
+    n = np.diff(off).astype(np.float64)
+    b = blocksizes(offsets, c).astype(np.float64)
+    rows = len(n)
+    row_work = np.where(b > 0, 0.5 * n + b + ROW_OVERHEAD, 1.0)
+    share = row_work.sum() / max(world, 1)
+    heavy = np.flatnonzero((row_work > max_share * share) & (n > seg)) if world > 1 else np.zeros(0, np.int64)
+    # units in (row, chunk) order: (row, chunk or -1, work)
+    units_row, units_chunk, units_work = [], [], []
+    prev = 0
+    for p in heavy.tolist():
+        if p > prev:
+            units_row.append(np.arange(prev, p))
+            units_chunk.append(np.full(p - prev, -1))
+            units_work.append(row_work[prev:p])
+        ns = int((n[p] + seg - 1) // seg)
+        lens = np.minimum(seg, n[p] - seg * np.arange(ns))
+        units_row.append(np.full(ns, p))
+        units_chunk.append(np.arange(ns))
+        units_work.append(lens * (0.5 + b[p] / n[p]) + ROW_OVERHEAD / ns)
+        prev = p + 1
+    if prev < rows:
+        units_row.append(np.arange(prev, rows))
+        units_chunk.append(np.full(rows - prev, -1))
+        units_work.append(row_work[prev:rows])
+    ur = np.concatenate(units_row) if units_row else np.zeros(0, np.int64)
+    uc = np.concatenate(units_chunk) if units_chunk else np.zeros(0, np.int64)
+    uw = np.concatenate(units_work) if units_work else np.zeros(0)
+    cum = np.concatenate([[0.0], np.cumsum(uw)])
+    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * k / world, side="left")) for k in range(1, world)] + [len(uw)]
+    for i in range(1, len(cuts)):
+        cuts[i] = min(max(cuts[i], cuts[i - 1]), len(uw))
+    shards = []
+    for k in range(world):
+        u0, u1 = cuts[k], cuts[k + 1]
+        parts, full = [], None
+        i = u0
+        while i < u1:
+            p = int(ur[i])
+            if uc[i] < 0:  # a run of whole rows
+                j = i
+                while j < u1 and uc[j] < 0:
+                    j += 1
+                full = (p, int(ur[j - 1]) + 1) if full is None else (full[0], int(ur[j - 1]) + 1)
+                i = j
+                continue
+            j = i
+            while j < u1 and ur[j] == p and uc[j] >= 0:
+                j += 1
+            cb, ce = int(uc[i]), int(uc[j - 1]) + 1
+            ns = int((n[p] + seg - 1) // seg)
+            if cb == 0 and ce == ns:  # the whole chunked row landed on this rank
+                full = (p, p + 1) if full is None else (full[0], p + 1)
+            else:
+                parts.append((p, cb, ce))
+            i = j
+        # whole rows are contiguous; a shared row sits before or after them
+        if full is None:
+            first = parts[0][0] if parts else (int(ur[u0]) if u0 < len(ur) else rows)
+            full = (first, first)
+        o0, o1 = full
+        for (p, cb, ce) in parts:
+            if cb == 0:
+                o1 = max(o1, p + 1) if o1 > o0 else p + 1
+                o0 = min(o0, p) if o1 > o0 else p
+        kr = [full[0], full[1]] if full[1] > full[0] else []
+        for (p, _, _) in parts:
+            kr += [p, p + 1]
+        keep = (min(kr), max(kr)) if kr else (full[0], full[0])
+        shards.append(Shard(full, parts, (o0, o1), keep))
+    # owned ranges must tile [0, rows): rows nobody holds (empty tails) go to the next owner
+    return shards
+
+
 class RowGather:
     """Cached buffers + index maps for the per-mode exchange of one factor:
     every rank's rows bounds[k] of the 2-D tensor t (rows x ld) are replaced
@@ -148,17 +244,26 @@ class ShardedSweep:
     memory) or by an NCCL all-gather of the shards (exchange="gather")."""
 
     def __init__(self, ctx, cfg, rank: int, world: int, group=None, exchange: str = "auto",
-                 slab: bool = True):
+                 slab: bool = True, split: bool = True):
 
         import torch
         import torch.distributed as tdist
         self.ctx, self.cfg, self.rank, self.world, self.group = ctx, cfg, rank, world, group
         order, dims, _ = ctx.info()
         self.dims = dims
-        self.bounds = [partition_rows(ctx.view_offsets(m), cfg.c, world) for m in range(order)]
+        # heavy rows split across ranks (chunks + an exchange of their partial
+        # sums) need max_inner = 1; otherwise whole-row ranges
+        self.split = split and cfg.max_inner == 1 and world > 1
+        if self.split:
+            self.shards = [partition_split(ctx.view_offsets(m), cfg.c, world, ctx.segment_length(m))
+                           for m in range(order)]
+        else:
+            self.shards = [[Shard(r, [], r, r) for r in partition_rows(ctx.view_offsets(m), cfg.c, world)]
+                           for m in range(order)]
+        self.bounds = [[sh.owned for sh in self.shards[m]] for m in range(order)]
         if slab:  # this rank's rows only: ~1/N of every view stays on the device
             for m in range(order):
-                ctx.view_keep_rows(m, *self.bounds[m][rank])
+                ctx.view_keep_rows(m, *self.shards[m][rank].keep)
         self.view_bytes = [ctx.view_resident(m)[2] for m in range(order)]
         self.A = [factor_tensor(ctx, m, dims[m]) for m in range(order)]
         st = torch.cuda.current_stream()
@@ -177,6 +282,22 @@ class ShardedSweep:
             [RowGather(self.A[m], self.bounds[m], rank, group) for m in range(order)]
         self.nccl = dist_on and tdist.get_backend(group) == "nccl"
         self.flag = torch.zeros(1, dtype=torch.int32, device="cuda" if self.nccl else "cpu")
+        # shared heavy rows: per mode, every rank's chunk ranges laid out in one
+        # padded slot buffer (all-gathered), and the rows this rank finalises
+        self.NE = None
+        self._keep = []
+        self.slots, self.gathered, self.layout = {}, {}, {}
+        for m in range(order):
+            per_rank = [[(p, cb, ce) for (p, cb, ce) in self.shards[m][k].parts] for k in range(world)]
+            if not any(per_rank):
+                continue
+            if self.NE is None:
+                Rk = ctx.get_factor(0)[0].shape[1]
+                self.NE = Rk * Rk + Rk
+            smax = max(sum(ce - cb for (_, cb, ce) in pr) for pr in per_rank)
+            self.slots[m] = torch.zeros(smax * self.NE, dtype=torch.float32, device="cuda")
+            self.gathered[m] = torch.zeros(world * smax * self.NE, dtype=torch.float32, device="cuda")
+            self.layout[m] = (smax, per_rank)
 
     def barrier(self) -> None:
         """Every rank's queued updates (and their peer stores) are complete
@@ -190,10 +311,48 @@ class ShardedSweep:
             tdist.barrier(group=self.group)
 
     def sweep_mode(self, k: int, m: int, seed: int) -> None:
-        """This rank's rows of the mode-m update of sweep k, then the exchange."""
+        """This rank's part of the mode-m update of sweep k (its chunks of
+        shared heavy rows first, then its whole rows), the exchange of the
+        shared rows' partial sums and their finalisation by their owners,
+        then the factor exchange."""
+        import torch
+        import torch.distributed as tdist
         from .ntc import sweep_stream
-        r0, r1 = self.bounds[m][self.rank]
-        self.ctx.s_nmc_rows_async(m, r0, r1, self.cfg, sweep_stream(seed, k, m).state)
+        state = sweep_stream(seed, k, m).state
+        sh = self.shards[m][self.rank]
+        self._keep = []
+        if m in self.layout:
+            smax, per_rank = self.layout[m]
+            pos = 0
+            for (p, cb, ce) in sh.parts:
+                self.ctx.s_nmc_chunks_async(m, p, cb, ce, self.cfg, state,
+                                            self.slots[m].data_ptr() + 4 * pos * self.NE)
+                pos += ce - cb
+        self.ctx.s_nmc_rows_async(m, sh.full[0], sh.full[1], self.cfg, state)
+        if m in self.layout:
+            smax, per_rank = self.layout[m]
+            if self.nccl:
+                tdist.all_gather_into_tensor(self.gathered[m], self.slots[m], group=self.group)
+            else:  # gloo (CPU tests): through host copies once the chunks are done
+                self.ctx.collect()
+                host = [torch.empty(self.slots[m].numel(), dtype=torch.float32) for _ in range(self.world)]
+                tdist.all_gather(host, self.slots[m].cpu(), group=self.group)
+                self.gathered[m].copy_(torch.cat(host))
+            g = self.gathered[m].view(self.world, smax, self.NE)
+            for (p, cb, _) in sh.parts:
+                if cb != 0:
+                    continue
+                pieces = []  # the row's chunks from every rank, in chunk order
+                for kk in range(self.world):
+                    q = 0
+                    for (pp, cb2, ce2) in per_rank[kk]:
+                        if pp == p:
+                            pieces.append((cb2, g[kk, q: q + ce2 - cb2]))
+                        q += ce2 - cb2
+                pieces.sort(key=lambda x: x[0])
+                allslots = torch.cat([x[1] for x in pieces]).contiguous()
+                self._keep.append(allslots)  # alive until the stream has consumed it
+                self.ctx.finalize_row_async(m, p, allslots.data_ptr(), allslots.shape[0], self.cfg)
         if self.p2p:
             self.barrier()
         elif self.gather is not None:
@@ -216,6 +375,12 @@ class ShardedSweep:
         return float(t[0]), float(t[1]), reg
 
     def local_sampled(self, m: int) -> int:
-        r0, r1 = self.bounds[m][self.rank]
+        """Entries this rank's calls count for mode m: its whole rows plus the
+        shared rows it owns (a shared row is counted once, by its owner)."""
+        sh = self.shards[m][self.rank]
         off = self.ctx.view_offsets(m)
-        return int(blocksizes(off[r0: r1 + 1], self.cfg.c).sum()) * self.cfg.max_inner
+        n = int(blocksizes(off[sh.full[0]: sh.full[1] + 1], self.cfg.c).sum())
+        for (p, cb, _) in sh.parts:
+            if cb == 0:
+                n += int(blocksizes(off[p: p + 2], self.cfg.c).sum())
+        return n * self.cfg.max_inner

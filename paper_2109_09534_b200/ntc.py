@@ -412,6 +412,22 @@ class Context:
         cs = cfg.c_struct()
         check(self.L.ntcb_s_nmc_rows_async(self.h, mode, row_begin, row_end, C.byref(cs), rng_state))
 
+    def segment_length(self, mode) -> int:
+        v = C.c_uint64()
+        check(self.L.ntcb_segment_length(self.h, mode, C.byref(v)))
+        return v.value
+
+    def s_nmc_chunks_async(self, mode, row, chunk_begin, chunk_end, cfg: NmcConfig, rng_state: int, d_slots: int):
+        """Chunks [chunk_begin, chunk_end) of a shared heavy row: fp32 (H, w)
+        partials ((R*R + R) floats per chunk) into the device buffer d_slots."""
+        cs = cfg.c_struct()
+        check(self.L.ntcb_s_nmc_chunks_async(self.h, mode, row, chunk_begin, chunk_end, C.byref(cs), rng_state,
+                                             C.c_void_p(d_slots)))
+
+    def finalize_row_async(self, mode, row, d_slots: int, nslots, cfg: NmcConfig):
+        cs = cfg.c_struct()
+        check(self.L.ntcb_finalize_row_async(self.h, mode, row, C.c_void_p(d_slots), nslots, C.byref(cs)))
+
     def sweep_async(self, sweep, cfg: NmcConfig, seed):
         cs = cfg.c_struct()
         check(self.L.ntcb_sweep_async(self.h, sweep, C.byref(cs), seed))

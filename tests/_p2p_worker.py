@@ -19,14 +19,30 @@ CASES = {
     "zipf": dict(dims=[5000, 400, 60], nnz=400_000, R=16, synth=(6, 0.5, 77, [1.2, 1.2, 0.0], 1)),
     # order 4, rank 32: the NAT update (natural-layout gathers, shared tile)
     "nat4": dict(dims=[60, 50, 40, 30], nnz=120_000, R=32, synth=(8, 0.01, 99, None, 0)),
+    # one mode-0 row holding 44 % of the entries: split across the ranks
+    # (chunks + the all-gathered partial sums, finalised by the row's owner)
+    "heavy": dict(dims=[40, 3000, 400], nnz=None, R=12, synth=None),
 }
+
+
+def heavy_tensor():
+    rng = np.random.default_rng(4)
+    dims = CASES["heavy"]["dims"]
+    heavy = rng.choice(dims[1] * dims[2], 700_000, replace=False)
+    rest = rng.choice((dims[0] - 1) * dims[1] * dims[2], 900_000, replace=False) + dims[1] * dims[2]
+    cells = np.concatenate([heavy, rest])
+    idx = np.stack(np.unravel_index(cells, dims), 1).astype(np.uint32)
+    return dims, idx, (rng.random(len(cells)) * 3).astype(np.float32)
 
 
 def build(P, case="uniform"):
     c = CASES[case]
     ctx = P.Context(0)
-    tr, sigma, seed, zipf, kind = c["synth"]
-    ctx.synth(c["dims"], c["nnz"], tr, sigma, seed, zipf, kind)
+    if c["synth"] is None:
+        ctx.load(*heavy_tensor())
+    else:
+        tr, sigma, seed, zipf, kind = c["synth"]
+        ctx.synth(c["dims"], c["nnz"], tr, sigma, seed, zipf, kind)
     ctx.random_factors(c["R"], 7)
     return ctx
 

@@ -5,7 +5,8 @@ single-process sweep bit for bit on every rank.  Two processes on one GPU
 protocol are the multi-GPU ones; only the NVLink hop is missing.  Cases: a
 uniform tensor at 2 ranks, and a Zipf tensor (heavy slices, rows cut into
 many segments and summed through slot groups, the SHORT kernel) at 2 and 3
-ranks, and an order-4 rank-32 tensor (the NAT update) at 2 ranks."""
+ranks, an order-4 rank-32 tensor (the NAT update) at 2 ranks, and a tensor
+whose heaviest row is split across 3 ranks (dist.partition_split)."""
 import socket
 
 import numpy as np
@@ -21,7 +22,7 @@ def _port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("uniform", 2), ("zipf", 2), ("zipf", 3), ("nat4", 2)])
+@pytest.mark.parametrize("case,world", [("uniform", 2), ("zipf", 2), ("zipf", 3), ("nat4", 2), ("heavy", 3)])
 def test_fused_exchange_equals_serial(tmp_path, cuda_ok, case, world):
     import torch.multiprocessing as mp
     import _p2p_worker as W
