@@ -67,21 +67,30 @@ class Shard:
         return f"Shard(full={self.full}, parts={self.parts}, owned={self.owned}, keep={self.keep})"
 
 
-def partition_split(offsets: np.ndarray, c: float, world: int, seg: int, max_share: float = 0.5) -> List[Shard]:
+def partition_split(offsets: np.ndarray, c: float, world: int, seg: int, max_share: float = 1.0,
+                    max_split_n: int = 1 << 24) -> List[Shard]:
     """Contiguous ranges over work units balancing sum(n_p/2 + b_p) (+ a
     per-row overhead), where a unit is a whole row -- or, for a row whose
     work exceeds max_share of a rank's share, each of its chunks (seg
     entries from the row start, the library's segment_length).  A heavy row
     can so be split across ranks: every sharing rank computes its chunks'
     partial sums and the owner (chunk 0) sums all of them in chunk order --
-    the association of a single-GPU run, so results stay bitwise identical."""
+    the association of a single-GPU run, so results stay bitwise identical.
+    Every sharing rank samples the whole row (at c = 0.5 sampling a heavy
+    row costs about as much as updating it), so only rows that alone exceed
+    a rank's share are split by default, and rows above max_split_n entries
+    (the sampler's giant path) never: measured with tools/shard_probe.py at
+    8 ranks, splitting config 5's 261M-entry slice took its ranks from 8.4
+    to 9.9 ms, and splitting every row above 1/4 of a share moved config 3
+    from 1.46 to 1.54 ms but config 5 from 20.8 to 20.0 ms per sweep."""
     off = np.asarray(offsets, np.int64)
     n = np.diff(off).astype(np.float64)
     b = blocksizes(offsets, c).astype(np.float64)
     rows = len(n)
     row_work = np.where(b > 0, 0.5 * n + b + ROW_OVERHEAD, 1.0)
     share = row_work.sum() / max(world, 1)
-    heavy = np.flatnonzero((row_work > max_share * share) & (n > seg)) if world > 1 else np.zeros(0, np.int64)
+    heavy = np.flatnonzero((row_work > max_share * share) & (n > seg) & (n <= max_split_n)) if world > 1 \
+        else np.zeros(0, np.int64)
     # units in (row, chunk) order: (row, chunk or -1, work)
     units_row, units_chunk, units_work = [], [], []
     prev = 0

@@ -22,7 +22,7 @@ def test_partition_split_covers_everything_once(world, seg):
     off = _offsets(world * 7 + seg)
     n = np.diff(off.astype(np.int64))
     rows = len(n)
-    shards = partition_split(off, 0.5, world, seg)
+    shards = partition_split(off, 0.5, world, seg, max_share=0.5)
     assert len(shards) == world
     row_hits = np.zeros(rows, np.int64)
     chunk_hits = {}
@@ -53,7 +53,7 @@ def test_partition_split_covers_everything_once(world, seg):
     for p in shared:
         owner = [r for r, sh in enumerate(shards) if any(pp == p and cb == 0 for (pp, cb, _) in sh.parts)]
         assert len(owner) == 1 and owned[owner[0]][0] <= p < owned[owner[0]][1]
-    if world >= 3:  # the 1.2M-entry row is far above one rank's share: it must be shared
+    if world >= 3:  # the 1.2M-entry row is above one rank's share: it must be shared
         assert 1500 in shared
 
 
@@ -62,7 +62,7 @@ def test_partition_split_balances_work():
     n = np.diff(off.astype(np.int64)).astype(float)
     b = blocksizes(off, 0.5).astype(float)
     world, seg = 8, 2048
-    shards = partition_split(off, 0.5, world, seg)
+    shards = partition_split(off, 0.5, world, seg, max_share=0.5)
 
     def work(sh):
         w = float((0.5 * n[sh.full[0]:sh.full[1]] + b[sh.full[0]:sh.full[1]]).sum())
