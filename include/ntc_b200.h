@@ -117,6 +117,8 @@ typedef struct ntcb_tuning {
   int32_t heavy_win_log2;    /* log2 of the heavy sampler's draw window (24) */
   int32_t heavy_big_log2;    /* log2 of the slice length taking the windowed path (24) */
   int32_t host_threads;      /* host threads for fp64 <-> fp32 factor conversion, 0 = min(cores, 16) */
+  int32_t update_ctas_per_sm; /* resident update CTAs per SM (0 = as many as fit): fewer leave room
+                                for the side-stream sampler of the next mode to run alongside */
   int32_t update_carveout;   /* shared-memory carve-out preference (percent) of the update kernels,
                                 -1 = driver default; a smaller carve-out leaves more L1 for the
                                 in-flight factor-row gathers at the cost of resident CTAs */

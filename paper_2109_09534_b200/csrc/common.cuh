@@ -110,6 +110,7 @@ inline ntcb_tuning default_tuning() {
   t.heavy_win_log2 = 24;
   t.heavy_big_log2 = 24;
   t.host_threads = 0;
+  t.update_ctas_per_sm = 0;
   t.update_carveout = -1;
   t.peer_fence = 1;
   t.graph = 0;

@@ -1457,6 +1457,7 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
                                  ctx->tune.update_carveout));
   int per_sm = 0;
   NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT, SHORT>, wpc * 32, smem));
+  if (ctx->tune.update_ctas_per_sm > 0) per_sm = std::min(per_sm, ctx->tune.update_ctas_per_sm);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (pl.n_items + wpc - 1) / wpc;
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
