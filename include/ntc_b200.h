@@ -131,6 +131,10 @@ typedef struct ntcb_tuning {
                                 update; 1 on, 0 off, -1 (default) when the factors exceed 16 MB
                                 (gathers mostly miss L1: configs 3 and 5 measured 2.6 % / 5 % faster,
                                 configs 1 and 2, whose factors stay cached, slower) */
+  int32_t item_order;        /* work-list order of equally long update items: 0 row-major (a row's chunks
+                                together), 1 chunk-major (chunk s of every row together: co-resident
+                                warps gather the same window of the slowest-varying other factor, so
+                                its rows hit L1) */
 } ntcb_tuning;
 void ntcb_tuning_defaults(ntcb_tuning* t);
 int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t);

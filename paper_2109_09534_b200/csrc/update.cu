@@ -1352,9 +1352,21 @@ static WorkPlan& plan_for(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1,
     }
   }
   // longest items first: better tail balance for the dynamic scheduler
-  std::stable_sort(items.begin(), items.end(), [](const WorkItem& x, const WorkItem& y) {
-    return (x.e1 - x.e0) > (y.e1 - y.e0);
-  });
+  if (ctx->tune.item_order == 1) {
+    // chunk-major among equal lengths: chunk s of every row is scheduled
+    // together, so the warps resident on an SM walk the same window of the
+    // slowest-varying other coordinate and its factor rows hit L1 (the order
+    // of the items never changes a result: every item owns its slot)
+    std::stable_sort(items.begin(), items.end(), [&](const WorkItem& x, const WorkItem& y) {
+      const uint64_t lx = x.e1 - x.e0, ly = y.e1 - y.e0;
+      if (lx != ly) return lx > ly;
+      return (x.e0 - off[x.row]) < (y.e0 - off[y.row]);
+    });
+  } else {
+    std::stable_sort(items.begin(), items.end(), [](const WorkItem& x, const WorkItem& y) {
+      return (x.e1 - x.e0) > (y.e1 - y.e0);
+    });
+  }
   WorkPlan pl;
   pl.n_items = items.size();
   std::stable_partition(fins.begin(), fins.end(), [](const FinItem& f) { return f.nslots <= kFinSmall; });
