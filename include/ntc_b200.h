@@ -245,6 +245,14 @@ int ntcb_s_nmc(ntcb_context* ctx, int mode, const double* a_init, const ntcb_nmc
 int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a_out,
                     double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
                     uint64_t* entries_accessed);
+/* Optional hint for drivers built on ntcb_s_nmc / ntcb_s_nmc_host: the
+ * sampled set of a FUTURE call's first inner iteration (same mode, cfg->c
+ * and rng_state) is drawn now, on the sampler stream, while earlier work
+ * runs -- the sets depend on the stream state only (nmc.cpp:44-63), never
+ * on the factors, and ao_ntc's states are known ahead (sweep_stream,
+ * ao.cpp:65-68).  The matching call consumes it; any other sampling of the
+ * mode in between discards it.  Results are identical with or without. */
+int ntcb_sample_prefetch(ntcb_context* ctx, int mode, const ntcb_nmc_config* cfg, uint64_t rng_state);
 /* Row shard [row_begin, row_end) of the same update (multi-GPU partition;
  * rows are independent, nmc.cpp:231).  a_init aliases factors[mode].
  * Asynchronous: errors and the count are collected by ntcb_collect(). */

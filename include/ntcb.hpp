@@ -151,6 +151,13 @@ class Solver {
     return factor(mode);
   }
 
+  // Optional hint: draw the first sampled set of a later s_nmc(mode, ..., cfg, rng)
+  // now, while earlier work runs (ntcb_sample_prefetch); results are unchanged.
+  void sample_prefetch(int mode, const NmcConfig& cfg, RngStream rng) {
+    const ntcb_nmc_config c = cfg.c_config();
+    check(ntcb_sample_prefetch(ctx_, mode, &c, rng.state()));
+  }
+
   // ntc::ao_ntc (ao.cpp:75-133) on the loaded tensor; the factors are the init.
   std::vector<MetricsRecord> ao_ntc(const AoConfig& cfg,
                                     const std::function<void(const MetricsRecord&)>& obs = {}) {

@@ -116,6 +116,7 @@ SIGNATURES = {
     "ntcb_ipc_open": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "ntcb_factor_set_peers": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ntcb_s_nmc": (C.c_int, [C.c_void_p, C.c_int, f64p, C.POINTER(NmcConfigC), C.c_uint64, u64p]),
+    "ntcb_sample_prefetch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(NmcConfigC), C.c_uint64]),
     "ntcb_s_nmc_host": (C.c_int, [C.c_void_p, C.c_int, f64p, f64p, f64p, C.POINTER(NmcConfigC),
                                   C.c_uint64, u64p]),
     "ntcb_s_nmc_rows_async": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64,

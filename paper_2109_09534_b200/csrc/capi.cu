@@ -74,8 +74,20 @@ struct HostState {
   void* io_out = nullptr;
   uint64_t io_in_cap = 0, io_f_cap = 0, io_out_cap = 0;  // bytes
   bool queued = false;     // work enqueued since the last collect
+  // ntcb_sample_prefetch: the whole-mode sampled set of inner iteration 0 drawn ahead
+  struct Prefetch {
+    bool valid = false;
+    uint64_t rng_state = 0;
+    double c = 0.0;
+    int parity = 0;
+  } prefetch[NTCB_MAX_ORDER];
 };
 HostState& host_of(ntcb_context* ctx) { return *static_cast<HostState*>(ctx->host); }
+// prefetched sampled sets die with the masks / views / plans they were drawn for
+void drop_prefetch(ntcb_context* ctx) {
+  if (ctx->host)
+    for (auto& p : host_of(ctx).prefetch) p.valid = false;
+}
 
 #define API_TRY try {
 #define API_CATCH                                   \
@@ -169,6 +181,7 @@ int enqueue_sample(ntcb_context* ctx, int mode, uint64_t r0, uint64_t r1, const 
                    uint64_t rng_state, int l) {
   const int par = ctx->mask_parity[mode];
   ctx->mask_parity[mode] ^= 1;
+  host_of(ctx).prefetch[mode].valid = false;  // its buffer is the next one to be overwritten
   const DeviceView& v = ctx->views[mode];
   const uint64_t e0 = v.h_off[r0], e1 = v.h_off[r1];
   if (cfg.c < 1.0 && e1 > e0) {
@@ -510,6 +523,7 @@ void free_factors(ntcb_context* ctx) {
   }
   ctx->rank = ctx->ld = 0;
   ctx->nat_padded = false;
+  drop_prefetch(ctx);
   for (int m = 0; m < NTCB_MAX_ORDER; ++m) ctx->n_peers[m] = 0;
 }
 
@@ -728,6 +742,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
   if (t->update_carveout < -1 || t->update_carveout > 100)
     fail(NTCB_EINVAL, "tuning: update_carveout must be -1 or a percentage");
   collect(ctx, nullptr);  // queued work keeps the plans it was launched with
+  drop_prefetch(ctx);
   ctx->tune = *t;
   drop_plans(ctx);  // plans bake in the heavy-window sizes and the short-row decision
   drop_heavy(ctx);
@@ -925,6 +940,7 @@ int ntcb_view_keep_rows(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_
   need_rows(ctx, mode, row_begin, row_end);
   collect(ctx, nullptr);
   NTCB_CUDA(cudaStreamSynchronize(ctx->side));
+  drop_prefetch(ctx);
   DeviceView& v = ctx->views[mode];
   const int no = ctx->order - 1;
   const uint64_t e0 = v.h_off[row_begin], e1 = v.h_off[row_end];
@@ -1107,6 +1123,19 @@ int ntcb_factor_device_ptr(ntcb_context* ctx, int mode, int which, void** ptr, u
 
 // ntcb_s_nmc / ntcb_s_nmc_host: the host-buffer form enqueues the copies of
 // the updated factor and momentum before the call's single synchronisation
+// The prefetched sampled set of (mode, c, rng_state), if there is one: its
+// mask parity (the buffer stays reserved until the update has consumed it).
+static int take_prefetch(ntcb_context* ctx, int mode, const ntcb_nmc_config& cfg, uint64_t rng_state) {
+  auto& p = host_of(ctx).prefetch[mode];
+  if (!p.valid || p.rng_state != rng_state || p.c != cfg.c) return -1;
+  p.valid = false;
+  return p.parity;
+}
+static int sample_first(ntcb_context* ctx, int mode, const ntcb_nmc_config& cfg, uint64_t rng_state) {
+  const int pre = take_prefetch(ctx, mode, cfg, rng_state);
+  return pre >= 0 ? pre : enqueue_sample(ctx, mode, 0, ctx->dims[mode], cfg, rng_state, 0);
+}
+
 static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double* a_out, double* y_out,
                       bool outs, const ntcb_nmc_config* cfg, uint64_t rng_state, uint64_t* entries_accessed) {
   API_TRY
@@ -1125,7 +1154,7 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
   if (dev_io) {
     // page-locked caller buffers: a_init goes to the device as fp64 and is
     // checked and converted there; no host work on the critical path
-    if (cfg->max_inner > 0) pre = enqueue_sample(ctx, mode, 0, rows, *cfg, rng_state, 0);
+    if (cfg->max_inner > 0) pre = sample_first(ctx, mode, *cfg, rng_state);
     HostState& h = hs;
     double* din = io_buffer<double>(h.io_in, h.io_in_cap, rows * R);
     float* dsc = io_buffer<float>(h.io_f, h.io_f_cap, rows * ld);
@@ -1155,7 +1184,7 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
   if (a_init) {
     // the first sample does not read factors: it runs on the side stream
     // while a_init is converted and copied in
-    if (cfg->max_inner > 0) pre = enqueue_sample(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, 0);
+    if (cfg->max_inner > 0) pre = sample_first(ctx, mode, *cfg, rng_state);
     if (!upload_factor_async(ctx, ctx->A[mode], a_init, ctx->dims[mode])) {
       hs.verified[mode] = false;
       collect(ctx, nullptr);
@@ -1163,6 +1192,7 @@ static int s_nmc_impl(ntcb_context* ctx, int mode, const double* a_init, double*
     }
     hs.verified[mode] = true;
   }
+  if (!a_init && cfg->max_inner > 0) pre = take_prefetch(ctx, mode, *cfg, rng_state);
   const uint64_t own = enqueue_snmc_owned(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, pre);
   if (outs) download_factors_enqueue(ctx, mode, a_out != nullptr, y_out != nullptr);
   collect(ctx, nullptr);  // the one synchronisation of the call
@@ -1180,6 +1210,25 @@ int ntcb_s_nmc_host(ntcb_context* ctx, int mode, const double* a_init, double* a
                     double* y_out, const ntcb_nmc_config* cfg, uint64_t rng_state,
                     uint64_t* entries_accessed) {
   return s_nmc_impl(ctx, mode, a_init, a_out, y_out, true, cfg, rng_state, entries_accessed);
+}
+
+int ntcb_sample_prefetch(ntcb_context* ctx, int mode, const ntcb_nmc_config* cfg, uint64_t rng_state) {
+  API_TRY
+  need_ctx(ctx);
+  validate_nmc(cfg);
+  need_tensor(ctx);
+  if (mode < 0 || mode >= ctx->order) fail(NTCB_EINVAL, "s_nmc: mode out of range");
+  need_rows(ctx, mode, 0, ctx->dims[mode]);
+  if (cfg->max_inner < 1 || cfg->c >= 1.0) return NTCB_OK;  // nothing is drawn (c = 1 consumes no randomness)
+  auto& p = host_of(ctx).prefetch[mode];
+  const int par = enqueue_sample(ctx, mode, 0, ctx->dims[mode], *cfg, rng_state, 0);  // clears p.valid
+  p.valid = true;
+  p.rng_state = rng_state;
+  p.c = cfg->c;
+  p.parity = par;
+  // `queued` stays as it is: the matching s_nmc call must not drain the sampler first
+  // (every entry point that frees or replaces device state collects unconditionally)
+  API_CATCH
 }
 
 int ntcb_s_nmc_rows_async(ntcb_context* ctx, int mode, uint64_t row_begin, uint64_t row_end,
@@ -1281,6 +1330,7 @@ int ntcb_sample_rows(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
   NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * po[rows]));
   NTCB_CUDA(cudaMemcpy(d_po, po.data(), sizeof(uint64_t) * (rows + 1), cudaMemcpyHostToDevice));
   collect(ctx, nullptr);
+  host_of(ctx).prefetch[mode].valid = false;  // mask buffer 0 is overwritten below
   uint32_t* mask = ctx->mask[mode][0];
   const uint64_t e0 = off[row_begin], e1 = off[row_end];
   if (e1 > e0) {
@@ -1315,6 +1365,7 @@ int ntcb_sample_row(ntcb_context* ctx, int mode, uint64_t row, double c, uint64_
   NTCB_CUDA(cudaMalloc(&d_pk, sizeof(uint32_t) * b));
   NTCB_CUDA(cudaMemcpy(d_po, po, sizeof po, cudaMemcpyHostToDevice));
   collect(ctx, nullptr);
+  host_of(ctx).prefetch[mode].valid = false;  // mask buffer 0 is overwritten below
   uint32_t* mask = ctx->mask[mode][0];
   const uint64_t e0 = off[row], e1 = off[row + 1];
   const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
@@ -1341,6 +1392,7 @@ int ntcb_sample_mask(ntcb_context* ctx, int mode, double c, uint64_t rng_state, 
   const uint64_t* off = ctx->views[mode].h_off;
   const uint64_t e0 = off[row_begin], e1 = off[row_end];
   if (e1 <= e0) return NTCB_OK;
+  host_of(ctx).prefetch[mode].valid = false;  // mask buffer 0 is overwritten below
   uint32_t* mask = ctx->mask[mode][0];
   const uint64_t w0 = e0 >> 5, w1 = ((e1 - 1) >> 5) + 1;
   NTCB_CUDA(cudaMemsetAsync(mask + w0, 0, sizeof(uint32_t) * (w1 - w0), ctx->stream));

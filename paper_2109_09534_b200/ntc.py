@@ -408,6 +408,13 @@ class Context:
                                      C.byref(cs), rng_state, C.byref(acc)))
         return acc.value
 
+    def sample_prefetch(self, mode, cfg: NmcConfig, rng_state: int) -> None:
+        """Hint (ntcb_sample_prefetch): draw the first sampled set of a future
+        s_nmc / s_nmc_host call (same mode, c, rng_state) now, on the sampler
+        stream.  Results are unchanged."""
+        cs = cfg.c_struct()
+        check(self.L.ntcb_sample_prefetch(self.h, mode, C.byref(cs), rng_state))
+
     def s_nmc_rows_async(self, mode, row_begin, row_end, cfg: NmcConfig, rng_state: int):
         cs = cfg.c_struct()
         check(self.L.ntcb_s_nmc_rows_async(self.h, mode, row_begin, row_end, C.byref(cs), rng_state))

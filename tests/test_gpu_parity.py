@@ -312,6 +312,49 @@ def test_host_buffers_pinned_equals_pageable(ntc):
     ctx.s_nmc(1, cfg, 99)  # the context works normally afterwards
 
 
+def test_sample_prefetch_changes_nothing(ntc):
+    """ntcb_sample_prefetch (the sampled set of a future call drawn ahead on
+    the sampler stream) is consumed by the matching s_nmc / s_nmc_host call
+    and ignored otherwise; factors, momentum and counts are bitwise those of
+    calls without it."""
+    import paper_2109_09534_b200 as P
+    dims, R = [3000, 400, 50], 12
+    ctx = P.Context(0)
+    ctx.synth(dims, 1_000_000, 4, 0.01, 17)
+    cfg = P.NmcConfig(c=0.5)
+    st = [P.sweep_stream(11, 0, m).state for m in range(3)]
+
+    def run(prefetch):
+        ctx.random_factors(R, 3)
+        out = []
+        a0 = [P.pinned_like(ctx.get_factor(m)[0]) for m in range(3)]
+        ao = [P.pinned_like(np.zeros_like(a)) for a in a0]
+        yo = [P.pinned_like(np.zeros_like(a)) for a in a0]
+        if prefetch == "match":
+            ctx.sample_prefetch(0, cfg, st[0])
+        for m in range(3):
+            if prefetch == "match" and m + 1 < 3:
+                ctx.sample_prefetch(m + 1, cfg, st[m + 1])  # drawn while mode m updates
+            if prefetch == "stale":
+                ctx.sample_prefetch(m, cfg, st[m] ^ 1)      # another stream: must be ignored
+            if prefetch == "clobbered":
+                ctx.sample_prefetch(m, cfg, st[m])
+                ctx.sample_mask(m, 0.5, 77)                  # other sampling of the mode discards it
+            n = ctx.s_nmc_host(m, a0[m], ao[m], yo[m], cfg, st[m])
+            out.append((n, np.array(ao[m]), np.array(yo[m])))
+        n_dev = ctx.s_nmc(1, cfg, st[1]) if prefetch != "match" else (ctx.sample_prefetch(1, cfg, st[1]), ctx.s_nmc(1, cfg, st[1]))[1]
+        out.append((n_dev, *ctx.get_factor(1)))
+        return out
+
+    base = run(None)
+    for kind in ("match", "stale", "clobbered"):
+        got = run(kind)
+        for (n0, a, y), (n1, a1, y1) in zip(base, got):
+            assert n0 == n1
+            np.testing.assert_array_equal(a, a1)
+            np.testing.assert_array_equal(y, y1)
+
+
 def test_collect_counts_survive_internal_drains(ntc):
     """ntcb_collect returns the entries of every async sweep queued since the
     last collect, even when other calls (metrics, a blocking s_nmc, sampling)

@@ -343,7 +343,7 @@ static void bench(const float* dU1, const float* dU2, int rows, int R, int ctas_
 int main(int argc, char** argv) {
   cudaDeviceProp pr;
   CK(cudaGetDeviceProperties(&pr, 0));
-  const int rows = 10000;
+  const int rows = argc > 3 ? atoi(argv[3]) : 10000;  // factor rows (256: L1-resident gathers)
   std::vector<float> U1(static_cast<size_t>(rows) * 32), U2(U1.size());
   uint64_t s = 12345;
   auto rnd = [&]() {
