@@ -127,8 +127,10 @@ typedef struct ntcb_tuning {
   int32_t peer_fence;        /* ordering of the rows stored into peer replicas: 1 (default) one
                                 system-scope fence per thread at kernel exit, 2 one per row,
                                 0 none (the kernel boundary + the NCCL barrier alone) */
-  int32_t nat_pad;           /* ranks 9-24, orders 3-4: 128-byte factor rows + the natural-layout (NAT)
-                                update; 1 on, 0 off, -1 (default) when the factors exceed 16 MB
+  int32_t nat_pad;           /* ranks 9-24, orders 3-4: whole-line factor rows + the natural-layout (NAT)
+                                update -- 64-byte rows read by 4 lanes per pick up to rank 16, 128-byte
+                                rows read by 8 lanes above (2: 128-byte rows at every rank, the A/B
+                                reference); 1 on, 0 off, -1 (default) when the factors exceed 16 MB
                                 (gathers mostly miss L1: configs 3 and 5 measured 2.6 % / 5 % faster,
                                 configs 1 and 2, whose factors stay cached, slower) */
   int32_t item_order;        /* work-list order of equally long update items: 0 row-major (a row's chunks

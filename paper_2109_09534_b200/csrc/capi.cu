@@ -539,9 +539,10 @@ void alloc_factors(ntcb_context* ctx, uint64_t rank) {
   // nat_pad: 128-byte rows (one L1 line per gathered row) for the NAT update
   uint64_t fbytes = 0;
   for (int m = 0; m < ctx->order; ++m) fbytes += ctx->dims[m] * rank * 4;
-  const bool pad = ctx->tune.nat_pad == 1 || (ctx->tune.nat_pad == -1 && fbytes > (16ull << 20));
+  const bool pad = ctx->tune.nat_pad >= 1 || (ctx->tune.nat_pad == -1 && fbytes > (16ull << 20));
   ctx->nat_padded = pad && rank >= 9 && rank <= 24 && (ctx->order == 3 || ctx->order == 4);
-  if (ctx->nat_padded) ctx->ld = 32;
+  // ranks 9-16: 64-byte rows (four lanes per pick); 17-24: 128-byte rows
+  if (ctx->nat_padded) ctx->ld = (rank <= 16 && ctx->tune.nat_pad != 2) ? 16 : 32;
   for (int m = 0; m < ctx->order; ++m) {
     // + 32 floats: the tensor-core gather of the last row may read past it
     const size_t bytes = sizeof(float) * (ctx->dims[m] * ctx->ld + 32);
@@ -734,7 +735,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
   if (t->heavy_win_log2 < 16 || t->heavy_win_log2 > 30 || t->heavy_big_log2 < 16 || t->heavy_big_log2 > 30)
     fail(NTCB_EINVAL, "tuning: heavy_win_log2 / heavy_big_log2 must be in [16, 30]");
   if (t->host_threads < 0) fail(NTCB_EINVAL, "tuning: host_threads must be >= 0");
-  if (t->nat_pad < -1 || t->nat_pad > 1) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0 or 1");
+  if (t->nat_pad < -1 || t->nat_pad > 2) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0, 1 or 2");
   if (t->peer_fence < 0 || t->peer_fence > 2) fail(NTCB_EINVAL, "tuning: peer_fence must be 0, 1 or 2");
   if (t->graph != 0 && t->graph != 1) fail(NTCB_EINVAL, "tuning: graph must be 0 or 1");
   if (t->item_order != 0 && t->item_order != 1) fail(NTCB_EINVAL, "tuning: item_order must be 0 or 1");

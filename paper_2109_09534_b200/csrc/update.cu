@@ -705,7 +705,10 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
 // Khatri-Rao rows k go through an 8 x 32 shared tile into the fragment
 // layout; w = sum x k is accumulated on the CUDA cores in the natural
 // layout (no x column in the tiles, so 32 features fit 4 blocks).
-template <int P, int NO, bool NAT = false, bool SHORT = false>
+// LPP = lanes per pick of the NAT gathers: 8 (128-byte rows, ld = 32) or 4
+// (64-byte rows, ld = 16, ranks <= 16: eight picks per load instruction and
+// half the factor footprint in L2 -- configs 3 and 5, whose factors exceed L2).
+template <int P, int NO, bool NAT = false, bool SHORT = false, int LPP = 8>
 __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
@@ -740,7 +743,9 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
 #pragma unroll
   for (int f = 0; f < P; ++f)
     if (!NAT && feat(g, f) == R) xf = f;
-  const int nq = lane >> 3, nsub = lane & 7;  // NAT: pick slot (and +4), feature quad
+  constexpr int NPS = 32 / LPP;  // NAT: picks per load instruction
+  constexpr int NH = 8 / NPS;    // load instructions per group of 8 picks
+  const int nq = lane / LPP, nsub = lane % LPP;  // NAT: pick slot (and + NPS), feature quad
   const uint32_t ld4 = static_cast<uint32_t>(ld) * 4u;
 
   const float* ub2[NO];
@@ -843,16 +848,16 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       float x[2];
     };
     struct RawNat {
-      float4 v[2][NO];  // picks nq, nq + 4: features 4 nsub .. 4 nsub + 3 of each mode
-      float x[2];
+      float4 v[NH][NO];  // picks nq (, nq + 4): features 4 nsub .. 4 nsub + 3 of each mode
+      float x[NH];
     };
     using Raw = typename std::conditional<NAT, RawNat, RawPair>::type;
     float4 wacc = make_float4(0.f, 0.f, 0.f, 0.f);  // NAT: w = sum x k, features 4 nsub..+3
     auto load_nat = [&](int at, int np) {
       RawNat r;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = nq + 4 * h;
+      for (int h = 0; h < NH; ++h) {
+        const int q = nq + NPS * h;
         const bool on = q < np;
         const int sl = (at + q) & (W::kStage - 1);
 #pragma unroll
@@ -925,7 +930,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       if constexpr (NAT) {
         // natural layout -> products -> shared tile -> fragment layout
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NH; ++h) {
           float4 k = r.v[h][0];
 #pragma unroll
           for (int m = 1; m < NO; ++m)
@@ -939,7 +944,7 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
           wacc.y = fmaf(r.x[h], k.y, wacc.y);
           wacc.z = fmaf(r.x[h], k.z, wacc.z);
           wacc.w = fmaf(r.x[h], k.w, wacc.w);
-          *reinterpret_cast<float4*>(kt + (nq + 4 * h) * kKtStride + 4 * nsub) = k;
+          *reinterpret_cast<float4*>(kt + (nq + NPS * h) * kKtStride + 4 * nsub) = k;
         }
         __syncwarp();
 #pragma unroll
@@ -1099,9 +1104,9 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
       }
     }
     if constexpr (NAT) {
-      // w: sum the 4 pick slots holding the same features (lanes nsub + 8 q)
+      // w: sum the pick slots holding the same features (lanes nsub + LPP q)
 #pragma unroll
-      for (int o = 8; o < 32; o <<= 1) {
+      for (int o = LPP; o < 32; o <<= 1) {
         wacc.x += __shfl_xor_sync(0xffffffffu, wacc.x, o);
         wacc.y += __shfl_xor_sync(0xffffffffu, wacc.y, o);
         wacc.z += __shfl_xor_sync(0xffffffffu, wacc.z, o);
@@ -1143,6 +1148,11 @@ __global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(Upd
 // warp order in shared memory (deterministic: the association depends only
 // on the slot count) and warp 0 runs the same finalisation.
 constexpr int kFinPass = 512;  // elements per pass (16 per lane)
+// per-warp shared words of the finalise kernels: Hf (R x HS), then gd and vv
+// (64 doubles each).  (They used to carry the update kernel's whole per-warp
+// layout -- 9 KB at rank 20 -- which kept two thirds of the rows' warps off
+// the SMs: the row end is a chain of fp64 latencies, so residency is speed.)
+__host__ __device__ constexpr int fin_words(int R) { return WarpSmem<1>::ktile_words(R) + 64 * 2 * 2; }
 constexpr int kFinSmall = 16;  // rows with at most this many slots: a warp each
 
 template <int LD4>
@@ -1153,8 +1163,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize_small(UpdateArgs a) {
   const int wid = threadIdx.x >> 5;
   const int R = a.rank;
   const int HS = R | 1;
-  float* wbase = smem_f + static_cast<size_t>(wid) * W::words(a.no, R);
-  float* Hf = wbase + W::stage_words(a.no);
+  float* Hf = smem_f + static_cast<size_t>(wid) * fin_words(R);
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));
   double* vv = gd + 64;
   const int NE = R * R + R;
@@ -1242,10 +1251,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
   const int wid = threadIdx.x >> 5;
   const int R = a.rank;
   const int HS = R | 1;
-  float* Hf = smem_f + W::stage_words(a.no);  // warp 0's row-end buffers
+  float* Hf = smem_f;  // warp 0's row-end buffers
   double* gd = reinterpret_cast<double*>(Hf + W::ktile_words(R));
   double* vv = gd + 64;
-  double* P = reinterpret_cast<double*>(smem_f + W::words(a.no, R));  // [kWarps][kFinPass]
+  double* P = reinterpret_cast<double*>(smem_f + fin_words(R));  // [kWarps][kFinPass]
   const int NE = R * R + R;
   __shared__ int stop;
   for (uint64_t f = blockIdx.x; f < a.n_fins; f += gridDim.x) {
@@ -1452,7 +1461,7 @@ static int launch_items(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, si
   return 1;
 }
 
-template <int P, int NO, bool NAT = false, bool SHORT = false>
+template <int P, int NO, bool NAT = false, bool SHORT = false, int LPP = 8>
 static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_t smem) {
   // Few items (a small tensor or a thin row shard): fewer warps per CTA so the
   // items spread over every SM instead of filling a few.
@@ -1463,18 +1472,18 @@ static int launch_items_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl,
   const int wmax = ctx->tune.update_wpc;
   const int wpc = static_cast<int>(std::min<uint64_t>(wmax, std::max<uint64_t>(1, per_sm_items)));
   smem = warp_bytes * wpc;
-  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT, LPP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  NTCB_CUDA(cudaFuncSetAttribute(k_update_tc<P, NO, NAT, SHORT, LPP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  ctx->tune.update_carveout));
   int per_sm = 0;
-  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT, SHORT>, wpc * 32, smem));
+  NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_tc<P, NO, NAT, SHORT, LPP>, wpc * 32, smem));
   if (ctx->tune.update_ctas_per_sm > 0) per_sm = std::min(per_sm, ctx->tune.update_ctas_per_sm);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (pl.n_items + wpc - 1) / wpc;
   grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
   grid = std::max<uint64_t>(grid, 1);
-  k_update_tc<P, NO, NAT, SHORT><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
+  k_update_tc<P, NO, NAT, SHORT, LPP><<<static_cast<unsigned>(grid), wpc * 32, smem, ctx->stream>>>(a);
   NTCB_CUDA(cudaGetLastError());
   return 1;
 }
@@ -1490,8 +1499,7 @@ static int launch_tc(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl, size_
 // warp each), then slot groups and a CTA per row for the longer ones.
 template <int LD4>
 static int launch_finalize_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
-  using W = WarpSmem<LD4>;
-  const size_t smem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 * kWarps;
+  const size_t smem = static_cast<size_t>(fin_words(a.rank)) * 4 * kWarps;
   int launches = 0;
   if (pl.n_small) {  // warp per row
     NTCB_CUDA(cudaFuncSetAttribute(k_finalize_small<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1499,8 +1507,10 @@ static int launch_finalize_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& 
     UpdateArgs b = a;
     b.fins = pl.d_fins;
     b.n_fins = pl.n_small;
+    int per_sm = 0;
+    NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_small<LD4>, kWarps * 32, smem));
     const uint64_t fg = std::min<uint64_t>((pl.n_small + kWarps - 1) / kWarps,
-                                           static_cast<uint64_t>(ctx->sm_count) * 4);
+                                           static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1));
     k_finalize_small<LD4><<<static_cast<unsigned>(fg), kWarps * 32, smem, ctx->stream>>>(b);
     NTCB_CUDA(cudaGetLastError());
     ++launches;
@@ -1513,7 +1523,7 @@ static int launch_finalize_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& 
   }
   if (pl.n_fins > pl.n_small) {  // CTA per row
     // warp 0's row-end layout + the per-warp partial sums of one pass
-    const size_t fsmem = static_cast<size_t>(W::words(a.no, a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
+    const size_t fsmem = static_cast<size_t>(fin_words(a.rank)) * 4 + sizeof(double) * kWarps * kFinPass;
     NTCB_CUDA(cudaFuncSetAttribute(k_finalize<LD4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(fsmem)));
     UpdateArgs b = a;
@@ -1547,7 +1557,13 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // view (a property of the mode, not of a shard: the instantiation must not
   // depend on the partition) -- per-row latencies dominate there
   const bool short_rows = mode_short_rows(ctx, a.mode, a.c);
-  if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && (a.rank >= 25 || ctx->nat_padded) &&
+  if (pl.n_items && !g_tc_off && !nat_off && a.ld == 16 && ctx->nat_padded && a.rank <= 16 &&
+      (a.no == 2 || a.no == 3)) {
+    // ranks 9-16 on 64-byte rows: NAT with four lanes per pick
+    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true)) * 4 * kWarps;
+    launches += a.no == 2 ? launch_items_tc<2, 2, true, false, 4>(ctx, a, pl, ts)
+                          : launch_items_tc<2, 3, true, false, 4>(ctx, a, pl, ts);
+  } else if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && (a.rank >= 25 || ctx->nat_padded) &&
       (a.no == 2 || a.no == 3)) {
     // ranks 25-32 (and 9-24 with nat_pad's 128-byte rows): natural-layout
     // gathers through a shared tile into the tensor-core Gram (w on the CUDA

@@ -665,6 +665,44 @@ def test_ranks_and_orders_vs_oracle(ntc, orc, order, R):
             assert rel(y, M[m]) <= TOL, (k, m, rel(y, M[m]))
 
 
+@pytest.mark.parametrize("order,R,pad", [(3, 9, 1), (3, 12, 1), (3, 16, 1), (4, 16, 1), (3, 17, 1), (3, 24, 1),
+                                         (3, 16, 2), (4, 12, 2)])
+def test_nat_padded_rows_vs_oracle(ntc, orc, order, R, pad):
+    """ntcb_tuning.nat_pad (whole-line factor rows + natural-layout gathers:
+    64-byte rows read by 4 lanes per pick up to rank 16, 128-byte rows by 8
+    lanes above; pad = 2 forces 128-byte rows): the instantiations the auto
+    setting picks only when the factors exceed 16 MB, here on a small tensor
+    against the fp64 restatement, with short and split rows."""
+    import paper_2109_09534_b200 as P
+    rng = np.random.default_rng(order * 1000 + R * 10 + pad)
+    dims = [300, 40, 25] if order == 3 else [120, 30, 12, 6]
+    cells = int(np.prod(dims))
+    nnz = 120_000
+    lin = rng.choice(cells, nnz, replace=False)
+    idx = np.stack(np.unravel_index(lin, dims), 1).astype(np.uint32)
+    vals = (rng.random(nnz) * 2).astype(np.float32)
+    ctx = P.Context(0)
+    ctx.set_tuning(nat_pad=pad)
+    ctx.load(dims, idx, vals)
+    ci, cv = orc.canonicalize(dims, idx, vals.astype(np.float64))
+    views = [orc.build_view(dims, ci, cv, m) for m in range(order)]
+    F = [f.astype(np.float32).astype(np.float64) for f in orc.initial_factors(dims, R, 3)]
+    M = [f.copy() for f in F]
+    ctx.set_factors(R, F)
+    assert ctx.factor_device_ptr(0, 0)[1] == (16 if (R <= 16 and pad == 1) else 32)
+    for k in range(2):
+        ctx.sweep_async(k, P.NmcConfig(c=0.5, max_inner=1, lambda_=1e-2), 9)
+        acc = ctx.collect()
+        oacc = sum(orc.s_nmc(dims, R, F, M, m, views[m], None,
+                             O.nmc_cfg(c=0.5, max_inner=1, lambda_=1e-2, threads=8),
+                             orc.sweep_state(9, k, m)) for m in range(order))
+        assert acc == oacc
+        for m in range(order):
+            a, y = ctx.get_factor(m)
+            assert rel(a, F[m]) <= TOL, (k, m, rel(a, F[m]))
+            assert rel(y, M[m]) <= TOL, (k, m, rel(y, M[m]))
+
+
 def test_adaptive_segments_vs_oracle(ntc, orc):
     """Rows of 8000 entries in a range of 8M: the work list cuts them into
     2048-entry segments (partial slots + k_finalize) although they are below
