@@ -25,6 +25,7 @@ SOURCES = ["capi.cu", "tensor.cu", "sampler.cu", "update.cu", "metrics.cu", "syn
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+FLAGS += os.environ.get("NTCB_NVCC_EXTRA", "").split()  # experiment builds (tools/variants.sh), e.g. -DNTCB_NAT4_DEEP=4
 
 
 def _headers():
