@@ -685,6 +685,9 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
   return WarpSmem<1>::stage_words(no) > WarpSmem<1>::ktile_words(R) + 256 ? WarpSmem<1>::stage_words(no)
                                                                           : WarpSmem<1>::ktile_words(R) + 256;
 }
+#ifndef NTCB_NAT4_SHORT
+#define NTCB_NAT4_SHORT 1
+#endif
 constexpr int kKtStride = 36;          // natural layout: k' tile row stride (floats, bank-skewed)
 constexpr int kKtWords = 8 * kKtStride;  // 8 picks
 constexpr int kPreWords = 128;  // SHORT: [2 item parities][Y, A][32], the row's A and Y for the row end
@@ -1560,9 +1563,11 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   if (pl.n_items && !g_tc_off && !nat_off && a.ld == 16 && ctx->nat_padded && a.rank <= 16 &&
       (a.no == 2 || a.no == 3)) {
     // ranks 9-16 on 64-byte rows: NAT with four lanes per pick
-    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true)) * 4 * kWarps;
-    launches += a.no == 2 ? launch_items_tc<2, 2, true, false, 4>(ctx, a, pl, ts)
-                          : launch_items_tc<2, 3, true, false, 4>(ctx, a, pl, ts);
+    const bool shrt = short_rows && a.no == 2 && NTCB_NAT4_SHORT;
+    const size_t ts = static_cast<size_t>(tc_words(a.no, a.rank, true, shrt)) * 4 * kWarps;
+    launches += shrt        ? launch_items_tc<2, 2, true, true, 4>(ctx, a, pl, ts)
+                : a.no == 2 ? launch_items_tc<2, 2, true, false, 4>(ctx, a, pl, ts)
+                            : launch_items_tc<2, 3, true, false, 4>(ctx, a, pl, ts);
   } else if (pl.n_items && !g_tc_off && !nat_off && a.ld == 32 && (a.rank >= 25 || ctx->nat_padded) &&
       (a.no == 2 || a.no == 3)) {
     // ranks 25-32 (and 9-24 with nat_pad's 128-byte rows): natural-layout
