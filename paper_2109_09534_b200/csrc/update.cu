@@ -685,6 +685,13 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
   return WarpSmem<1>::stage_words(no) > WarpSmem<1>::ktile_words(R) + 256 ? WarpSmem<1>::stage_words(no)
                                                                           : WarpSmem<1>::ktile_words(R) + 256;
 }
+// Register budget of k_update_tc: 256 threads x 2 CTAs = 128 registers (4 CTAs of 4 warps per SM).  The
+// 4-way instantiations that gather three 16-byte pieces per pick slot (NAT on 128-byte rows, the quad
+// layout) spill at 128: they get 168 registers and 3 CTAs per SM instead (config 4: 60.0 -> 51.0 ms per
+// AO iteration).
+__host__ __device__ constexpr int tc_bound_threads(int P, int NO, bool NAT, int LPP) {
+  return (NO == 3 && ((NAT && LPP == 8) || P == 4)) ? 192 : kWarps * 32;
+}
 #ifndef NTCB_NAT4_SHORT
 #define NTCB_NAT4_SHORT 1
 #endif
@@ -712,7 +719,7 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
 // (64-byte rows, ld = 16, ranks <= 16: eight picks per load instruction and
 // half the factor footprint in L2 -- configs 3 and 5, whose factors exceed L2).
 template <int P, int NO, bool NAT = false, bool SHORT = false, int LPP = 8>
-__global__ void __launch_bounds__(kWarps * 32, (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
+__global__ void __launch_bounds__(tc_bound_threads(P, NO, NAT, LPP), (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
   constexpr int GP = 8;  // picks per group
