@@ -39,6 +39,9 @@
 
 namespace ntcb {
 
+#ifndef NTCB_ROW_END_REG
+#define NTCB_ROW_END_REG 1
+#endif
 constexpr int kWarps = 8;         // warps per CTA
 constexpr uint64_t kSeg = 16384;  // max entries per work item
 
@@ -264,6 +267,133 @@ __device__ void finalize_row(const UpdateArgs& a, uint64_t p, float* Hf, double*
     for (int q = 0; q < a.n_peers; ++q) a.peerA[q][p * ld + r] = static_cast<float>(an);
   }
   if (a.n_peers && a.peer_fence == 2) __threadfence_system();  // per row (A/B)
+}
+
+
+// The same row end for ranks up to RB <= 32 with each lane's row of H held in
+// REGISTERS: the mat-vecs of the gradient and of every power iteration read
+// Hf once instead of once per iteration, and v is read as 16-byte broadcasts
+// (two doubles per wavefront).  Same operations in the same order as
+// finalize_row -- identical results; on short-row modes (configs 3 and 5) the
+// row end was most of the kernel's shared-memory traffic.
+template <bool PRE, int RB>
+__device__ __forceinline__ void finalize_row_reg(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv,
+                                                 int lane, float y_pre = 0.f, float a_pre = 0.f) {
+  static_assert(RB % 4 == 0 && RB <= 32, "row block");
+  const int R = a.rank;
+  const int HS = R | 1;
+  const int ld = a.ld;
+  const double lam = a.lambda;
+  const bool mine = lane < R;
+  float hrow[RB];
+  bool hbad = false;
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    hrow[j] = (mine && j < R) ? Hf[lane * HS + j] : 0.f;
+    hbad |= !isfinite(hrow[j]);
+  }
+  const float yv = PRE ? y_pre : (mine ? a.Y[p * ld + lane] : 0.f);
+  const float av = PRE ? a_pre : (mine ? a.A[p * ld + lane] : 0.f);
+  if (mine) vv[lane] = static_cast<double>(yv);
+  __syncwarp();
+  const double2* v2 = reinterpret_cast<const double2*>(vv);
+  bool bad = false;
+  if (mine) {
+    double hy = 0.0;
+#pragma unroll
+    for (int j = 0; j < RB; j += 2) {
+      if (j < R) {
+        const double2 v = v2[j >> 1];
+        hy += static_cast<double>(hrow[j]) * v.x;
+        if (j + 1 < R) hy += static_cast<double>(hrow[j + 1]) * v.y;
+      }
+    }
+    gd[lane] = hy - gd[lane] + lam * static_cast<double>(yv);
+    bad = !isfinite(gd[lane]);
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 0);  // non-finite gradient
+    return;
+  }
+  if (__any_sync(0xffffffffu, hbad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 1);  // power_method rejects H
+    return;
+  }
+  const double v0 = 1.0 / sqrt(static_cast<double>(R));
+  __syncwarp();
+  if (mine) vv[lane] = v0;
+  __syncwarp();
+  double rq = 0.0, rq_prev = 0.0;
+  const int R4 = R & ~3;
+  for (int it = 0; it < a.power_iters; ++it) {
+    double u0 = 0.0;
+    if (mine) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int j = 0; j < RB; j += 4) {
+        if (j < R) {
+          const double2 va = v2[j >> 1];
+          const double2 vb = (j + 2 < R) ? v2[(j >> 1) + 1] : make_double2(0.0, 0.0);
+          if (j < R4) {
+            s0 += static_cast<double>(hrow[j]) * va.x;
+            s1 += static_cast<double>(hrow[j + 1]) * va.y;
+            s2 += static_cast<double>(hrow[j + 2]) * vb.x;
+            s3 += static_cast<double>(hrow[j + 3]) * vb.y;
+          } else {  // the last, partial quad goes to s0 in order (as finalize_row's tail loop)
+            s0 += static_cast<double>(hrow[j]) * va.x;
+            if (j + 1 < R) s0 += static_cast<double>(hrow[j + 1]) * va.y;
+            if (j + 2 < R) s0 += static_cast<double>(hrow[j + 2]) * vb.x;
+          }
+        }
+      }
+      u0 = ((s0 + s1) + (s2 + s3)) + lam * vv[lane];
+    }
+    double num = mine ? vv[lane] * u0 : 0.0, un2 = u0 * u0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      un2 += __shfl_xor_sync(0xffffffffu, un2, o);
+    }
+    rq = num;
+    if (un2 == 0.0) {
+      rq = 0.0;
+      break;
+    }
+    if (it > 0 && fabs(rq - rq_prev) <= a.power_tol * fabs(rq)) break;
+    rq_prev = rq;
+    const double inv = 1.0 / sqrt(un2);
+    __syncwarp();
+    if (mine) vv[lane] = u0 * inv;
+    __syncwarp();
+  }
+  const double L = rq * 1.01;  // nmc.cpp:253-254
+  if (!(L >= lam)) {
+    if (lane == 0) report(a.counters, a.mode, p, 2);  // row_step rejects L
+    return;
+  }
+  const double inv_l = 1.0 / L;
+  const double sl = sqrt(L), sm = sqrt(lam);
+  const double beta = (sl - sm) / (sl + sm);
+  if (mine) {
+    const double y = static_cast<double>(yv);
+    const double ap = static_cast<double>(av);
+    const double avn = y - inv_l * gd[lane];
+    const double an = avn > 0.0 ? avn : 0.0;
+    a.A[p * ld + lane] = static_cast<float>(an);
+    a.Y[p * ld + lane] = static_cast<float>(an + beta * (an - ap));
+    for (int q = 0; q < a.n_peers; ++q) a.peerA[q][p * ld + lane] = static_cast<float>(an);
+  }
+  if (a.n_peers && a.peer_fence == 2) __threadfence_system();  // per row (A/B)
+}
+
+// row end of rank <= RB (0: any rank)
+template <bool PRE, int RB>
+__device__ __forceinline__ void row_end(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv, int lane,
+                                        float y_pre = 0.f, float a_pre = 0.f) {
+  if constexpr (RB > 0 && RB <= 32 && NTCB_ROW_END_REG)
+    finalize_row_reg<PRE, RB>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
+  else
+    finalize_row<PRE>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
 }
 
 // The fused exchange's ordering (peer_fence 1, the default): every thread
@@ -1133,9 +1263,10 @@ __global__ void __launch_bounds__(tc_bound_threads(P, NO, NAT, LPP), (P <= 4 ? 2
     __syncwarp();
     if (cur.slot < 0) {
       if constexpr (SHORT)
-        finalize_row<true>(a, p, Hf, gd, vv, lane, lane < R ? my_pre[lane] : 0.f, lane < R ? my_pre[32 + lane] : 0.f);
+        row_end<true, (P <= 4 ? 8 * P : 0)>(a, p, Hf, gd, vv, lane, lane < R ? my_pre[lane] : 0.f,
+                                             lane < R ? my_pre[32 + lane] : 0.f);
       else
-        finalize_row(a, p, Hf, gd, vv, lane);
+        row_end<false, (P <= 4 ? 8 * P : 0)>(a, p, Hf, gd, vv, lane);
     } else {
       float* dst = a.partial + static_cast<uint64_t>(cur.slot) * (R * R + R);
       for (int i = lane; i < R * R; i += 32) dst[i] = Hf[(i / R) * HS + (i % R)];
@@ -1208,7 +1339,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize_small(UpdateArgs a) {
       }
     }
     __syncwarp();
-    finalize_row(a, fi.row, Hf, gd, vv, lane);
+    row_end<false, (LD4 <= 8 ? 4 * LD4 : 0)>(a, fi.row, Hf, gd, vv, lane);
     __syncwarp();
   }
   peer_fence_at_exit(a);
@@ -1305,7 +1436,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_finalize(UpdateArgs a) {
       }
       __syncthreads();
     }
-    if (wid == 0) finalize_row(a, fi.row, Hf, gd, vv, lane);
+    if (wid == 0) row_end<false, (LD4 <= 8 ? 4 * LD4 : 0)>(a, fi.row, Hf, gd, vv, lane);
     __syncthreads();
   }
   peer_fence_at_exit(a);
