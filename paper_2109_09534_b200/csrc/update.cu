@@ -819,6 +819,13 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
 // 4-way instantiations that gather three 16-byte pieces per pick slot (NAT on 128-byte rows, the quad
 // layout) spill at 128: they get 168 registers and 3 CTAs per SM instead (config 4: 60.0 -> 51.0 ms per
 // AO iteration).
+// ... and the short-row kernel on 64-byte rows (configs 3 and 5: the row end's fp64 latency chain
+// dominates) runs with 80 registers at 6 CTAs (24 warps) per SM: config 5 118.7 -> 112.6 ms, config 3
+// 6.18 -> 6.09 ms per AO iteration (64 registers spill: 123.5 / 6.54; the pair-layout short-row kernel
+// of config 1 loses at 80: 0.161 -> 0.187 ms, and keeps 128).
+__host__ __device__ constexpr int tc_bound_blocks(int P, bool SHORT, bool NAT, int LPP) {
+  return (SHORT && NAT && LPP == 4) ? 3 : (P <= 4 ? 2 : 1);
+}
 __host__ __device__ constexpr int tc_bound_threads(int P, int NO, bool NAT, int LPP) {
   return (NO == 3 && ((NAT && LPP == 8) || P == 4)) ? 192 : kWarps * 32;
 }
@@ -849,7 +856,7 @@ __device__ __forceinline__ const float* row_ptr(const float* base, uint32_t row,
 // (64-byte rows, ld = 16, ranks <= 16: eight picks per load instruction and
 // half the factor footprint in L2 -- configs 3 and 5, whose factors exceed L2).
 template <int P, int NO, bool NAT = false, bool SHORT = false, int LPP = 8>
-__global__ void __launch_bounds__(tc_bound_threads(P, NO, NAT, LPP), (P <= 4 ? 2 : 1)) k_update_tc(UpdateArgs a) {
+__global__ void __launch_bounds__(tc_bound_threads(P, NO, NAT, LPP), tc_bound_blocks(P, SHORT, NAT, LPP)) k_update_tc(UpdateArgs a) {
   using W = WarpSmem<1>;  // the per-warp layout does not depend on the rank blocking
   using G = TcGeo<P>;
   constexpr int GP = 8;  // picks per group
