@@ -822,7 +822,8 @@ __host__ __device__ constexpr int tc_ring_words(int no, int R) {
 // ... and the short-row kernel on 64-byte rows (configs 3 and 5: the row end's fp64 latency chain
 // dominates) runs with 80 registers at 6 CTAs (24 warps) per SM: config 5 118.7 -> 112.6 ms, config 3
 // 6.18 -> 6.09 ms per AO iteration (64 registers spill: 123.5 / 6.54; the pair-layout short-row kernel
-// of config 1 loses at 80: 0.161 -> 0.187 ms, and keeps 128).
+// of config 1 loses at 80: 0.161 -> 0.187 ms, and keeps 128; the long-row 64-byte-row kernel is
+// indifferent: 6.046 vs 6.045 ms at config 3).
 __host__ __device__ constexpr int tc_bound_blocks(int P, bool SHORT, bool NAT, int LPP) {
   return (SHORT && NAT && LPP == 4) ? 3 : (P <= 4 ? 2 : 1);
 }
