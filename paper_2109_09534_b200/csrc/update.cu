@@ -1304,8 +1304,9 @@ constexpr int kFinPass = 512;  // elements per pass (16 per lane)
 __host__ __device__ constexpr int fin_words(int R) { return WarpSmem<1>::ktile_words(R) + 64 * 2 * 2; }
 constexpr int kFinSmall = 16;  // rows with at most this many slots: a warp each
 
+// 64 registers: 4 CTAs (32 warps) per SM -- the kernel waits on its slot loads (config 2 4.71 -> 4.62 ms)
 template <int LD4>
-__global__ void __launch_bounds__(kWarps * 32) k_finalize_small(UpdateArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 4) k_finalize_small(UpdateArgs a) {
   using W = WarpSmem<LD4>;
   extern __shared__ __align__(16) float smem_f[];
   const int lane = threadIdx.x & 31;

@@ -1,7 +1,7 @@
 # The round-end measurement batch (run on the GPU box from the repo root):
 #   gpurun -- "bash tools/measure_round.sh TAG > gpurun_out/TAG_final.log 2>&1"
 # Outputs land in gpurun_out/TAG_*; summaries are copied into profiles/.
-TAG=${1:-r02}
+TAG=${1:-r02b}
 set -x
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
