@@ -1303,6 +1303,10 @@ constexpr int kFinPass = 512;  // elements per pass (16 per lane)
 // the SMs: the row end is a chain of fp64 latencies, so residency is speed.)
 __host__ __device__ constexpr int fin_words(int R) { return WarpSmem<1>::ktile_words(R) + 64 * 2 * 2; }
 constexpr int kFinSmall = 16;  // rows with at most this many slots: a warp each
+#ifndef NTCB_FINQ
+#define NTCB_FINQ 8
+#endif
+constexpr int kFinQ = NTCB_FINQ;  // slots whose loads are in flight together in k_finalize_small
 
 // 64 registers: 4 CTAs (32 warps) per SM -- the kernel waits on its slot loads (config 2 4.71 -> 4.62 ms)
 template <int LD4>
@@ -1321,20 +1325,21 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_finalize_small(UpdateArgs a)
     if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
     const FinItem fi = a.fins[f];
     const float* base = a.partial + static_cast<uint64_t>(fi.slot0) * NE;
-    // slot sums in slot order; the slot loads of 4 elements per lane are in flight together
+    // slot sums in slot order; the loads of kFinQ slots x 4 elements per lane are in flight together
+    // (rows of up to kFinQ slots -- config 2's five -- take one round of loads per 128 elements)
     for (int i0 = 0; i0 < NE; i0 += 128) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int q = 0; q < fi.nslots; q += 4) {
-        float v[4][4];
+      for (int q = 0; q < fi.nslots; q += kFinQ) {
+        float v[kFinQ][4];
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq)
+        for (int qq = 0; qq < kFinQ; ++qq)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int i = i0 + 32 * u + lane;
             v[qq][u] = (q + qq < fi.nslots && i < NE) ? base[static_cast<uint64_t>(q + qq) * NE + i] : 0.f;
           }
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq)
+        for (int qq = 0; qq < kFinQ; ++qq)
 #pragma unroll
           for (int u = 0; u < 4; ++u) acc[u] += static_cast<double>(v[qq][u]);
       }
