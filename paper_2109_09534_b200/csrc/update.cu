@@ -40,7 +40,7 @@
 namespace ntcb {
 
 #ifndef NTCB_ROW_END_REG
-#define NTCB_ROW_END_REG 1
+#define NTCB_ROW_END_REG 2
 #endif
 constexpr int kWarps = 8;         // warps per CTA
 constexpr uint64_t kSeg = 16384;  // max entries per work item
@@ -386,14 +386,126 @@ __device__ __forceinline__ void finalize_row_reg(const UpdateArgs& a, uint64_t p
   if (a.n_peers && a.peer_fence == 2) __threadfence_system();  // per row (A/B)
 }
 
+// Ranks up to 16: lane (r = lane % 16, h = lane / 16) holds HALF a row of H --
+// columns 8h .. 8h+7, as doubles -- so all 32 lanes work on the mat-vecs, a
+// lane reads half of v per product (two distinct 16-byte addresses per load
+// instruction instead of one broadcast: half the shared-memory wavefronts),
+// and the two reductions of a power iteration run over 16 lanes (both halves
+// identically: every lane sees the same sums, no divergence).  The row end is
+// most of the work on the short Zipf rows of configs 3 and 5.
+template <bool PRE>
+__device__ __forceinline__ void finalize_row_half(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv,
+                                                  int lane, const float* pre_y, const float* pre_a) {
+  const int R = a.rank;
+  const int HS = R | 1;
+  const int ld = a.ld;
+  const double lam = a.lambda;
+  const int r = lane & 15, h = lane >> 4;
+  const bool mine = r < R;
+  double hd[8];
+  bool hbad = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = 8 * h + j;
+    const float v = (mine && c < R) ? Hf[r * HS + c] : 0.f;
+    hbad |= !isfinite(v);
+    hd[j] = static_cast<double>(v);
+  }
+  const float yv = mine ? (PRE ? pre_y[r] : a.Y[p * ld + r]) : 0.f;
+  const float av = mine ? (PRE ? pre_a[r] : a.A[p * ld + r]) : 0.f;
+  __syncwarp();
+  if (lane < 16) vv[lane] = static_cast<double>(yv);  // zeros beyond R: the products below read all 16
+  __syncwarp();
+  const double2* v2 = reinterpret_cast<const double2*>(vv) + 4 * h;  // this lane's half of v
+  // (H + shift I) v, this lane's half: two chains over the even / odd columns
+  auto half_dot = [&]() {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const double2 v = v2[j >> 1];
+      s0 += hd[j] * v.x;
+      s1 += hd[j + 1] * v.y;
+    }
+    const double s = s0 + s1;
+    return s + __shfl_xor_sync(0xffffffffu, s, 16);  // + the other half: the same sum in both lanes
+  };
+  const double hy = half_dot();
+  double g = 0.0;
+  bool bad = false;
+  if (mine) {
+    g = hy - gd[r] + lam * static_cast<double>(yv);
+    bad = !isfinite(g);
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 0);  // non-finite gradient
+    return;
+  }
+  if (__any_sync(0xffffffffu, hbad)) {
+    if (lane == 0) report(a.counters, a.mode, p, 1);  // power_method rejects H
+    return;
+  }
+  const double v0 = 1.0 / sqrt(static_cast<double>(R));
+  double vr = mine ? v0 : 0.0;  // v_r, kept in a register too
+  __syncwarp();
+  if (lane < 16) vv[lane] = vr;
+  __syncwarp();
+  double rq = 0.0, rq_prev = 0.0;
+  for (int it = 0; it < a.power_iters; ++it) {
+    const double hv = half_dot();  // every lane takes part in its exchange
+    const double u = mine ? hv + lam * vr : 0.0;
+    double num = vr * u, un2 = u * u;
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {  // over the 16 lanes of a half; both halves hold the same values
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      un2 += __shfl_xor_sync(0xffffffffu, un2, o);
+    }
+    rq = num;
+    if (un2 == 0.0) {
+      rq = 0.0;
+      break;
+    }
+    if (it > 0 && fabs(rq - rq_prev) <= a.power_tol * fabs(rq)) break;
+    rq_prev = rq;
+    vr = u * (1.0 / sqrt(un2));
+    __syncwarp();
+    if (lane < 16) vv[lane] = vr;
+    __syncwarp();
+  }
+  const double L = rq * 1.01;  // nmc.cpp:253-254
+  if (!(L >= lam)) {
+    if (lane == 0) report(a.counters, a.mode, p, 2);  // row_step rejects L
+    return;
+  }
+  if (mine && h == 0) {
+    const double inv_l = 1.0 / L;
+    const double sl = sqrt(L), sm = sqrt(lam);
+    const double beta = (sl - sm) / (sl + sm);
+    const double y = static_cast<double>(yv);
+    const double ap = static_cast<double>(av);
+    const double avn = y - inv_l * g;
+    const double an = avn > 0.0 ? avn : 0.0;
+    a.A[p * ld + r] = static_cast<float>(an);
+    a.Y[p * ld + r] = static_cast<float>(an + beta * (an - ap));
+    for (int q = 0; q < a.n_peers; ++q) a.peerA[q][p * ld + r] = static_cast<float>(an);
+  }
+  if (a.n_peers && a.peer_fence == 2) __threadfence_system();  // per row (A/B)
+}
+
 // row end of rank <= RB (0: any rank)
+// (pre: SHORT's staged copies of the row, Y at pre[0..R), A at pre[32..32+R))
 template <bool PRE, int RB>
 __device__ __forceinline__ void row_end(const UpdateArgs& a, uint64_t p, float* Hf, double* gd, double* vv, int lane,
-                                        float y_pre = 0.f, float a_pre = 0.f) {
-  if constexpr (RB > 0 && RB <= 32 && NTCB_ROW_END_REG)
-    finalize_row_reg<PRE, RB>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
-  else
-    finalize_row<PRE>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
+                                        const float* pre = nullptr) {
+  if constexpr (RB > 0 && RB <= 16 && NTCB_ROW_END_REG == 2) {
+    finalize_row_half<PRE>(a, p, Hf, gd, vv, lane, pre, pre + 32);
+  } else {
+    const bool on = PRE && lane < a.rank;
+    const float y_pre = on ? pre[lane] : 0.f, a_pre = on ? pre[32 + lane] : 0.f;
+    if constexpr (RB > 0 && RB <= 32 && NTCB_ROW_END_REG)
+      finalize_row_reg<PRE, RB>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
+    else
+      finalize_row<PRE>(a, p, Hf, gd, vv, lane, y_pre, a_pre);
+  }
 }
 
 // The fused exchange's ordering (peer_fence 1, the default): every thread
@@ -1271,8 +1383,7 @@ __global__ void __launch_bounds__(tc_bound_threads(P, NO, NAT, LPP), tc_bound_bl
     __syncwarp();
     if (cur.slot < 0) {
       if constexpr (SHORT)
-        row_end<true, (P <= 4 ? 8 * P : 0)>(a, p, Hf, gd, vv, lane, lane < R ? my_pre[lane] : 0.f,
-                                             lane < R ? my_pre[32 + lane] : 0.f);
+        row_end<true, (P <= 4 ? 8 * P : 0)>(a, p, Hf, gd, vv, lane, my_pre);
       else
         row_end<false, (P <= 4 ? 8 * P : 0)>(a, p, Hf, gd, vv, lane);
     } else {
