@@ -21,6 +21,17 @@ __global__ void __launch_bounds__(256, 2) k(const float* __restrict__ U, const u
         float w = __ldg(b + 16 + g);
         acc += v.x * v.y + w;
       }
+    } else if (V == 9) {  // pair on a row-rotated layout: rows with row % 4 == 1 (byte offset 96 mod 128) store
+                          // features 16-23 first, so the 64-byte part never straddles an L1 line
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t row = r[2 * t + q];
+        const float* b = U + (size_t)row * LD;
+        const bool rot = (row & 3u) == 1u;
+        float2 v = __ldg(reinterpret_cast<const float2*>(b + (rot ? 8 : 0) + 2 * g));
+        float w = __ldg(b + (rot ? 0 : 16) + g);
+        acc += v.x * v.y + w;
+      }
     } else if (V == 2) {  // natural: 8 lanes per row, lanes g<6 float4
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -116,6 +127,7 @@ int main() {
   smem = sm_kb * 1024;
   printf("smem per CTA %d KB\n", sm_kb);
   run(k<1, 24>, "pair ld24 (LDG.64+LDG.32)");
+  run(k<9, 24>, "pair ld24, rotated rows (no straddle)");
   run(k<2, 24>, "natural ld24 float4");
   run(k<3, 24>, "scalar ld24 3xLDG.32");
   run(k<4, 24>, "natural ld24 float2");
