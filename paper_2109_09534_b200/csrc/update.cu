@@ -39,6 +39,9 @@
 
 namespace ntcb {
 
+// Compile-time A/B switches of tools/variants.sh (defaults = the measured best, profiles/r02_update_experiments.txt):
+// NTCB_ROW_END_REG 0 row end reads H from shared memory, 1 rows of H in registers, 2 + half rows up to rank 16;
+// NTCB_NAT4_SHORT  the short-row instantiation of the 64-byte-row NAT kernel; NTCB_FINQ slots in flight in k_finalize_small.
 #ifndef NTCB_ROW_END_REG
 #define NTCB_ROW_END_REG 2
 #endif
