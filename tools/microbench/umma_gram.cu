@@ -371,6 +371,7 @@ int main(int argc, char** argv) {
   bad += check<true>(U1, U2, dU1, dU2, rows, 20, 256, "item of 1024 picks");
   bad += check<true>(U1, U2, dU1, dU2, rows, 20, 4096, "item of 16384 picks (bias)");
   printf("checks failed: %d\n", bad);
+  if (argc > 1 && !strcmp(argv[1], "check")) return bad;  // correctness part only (tests/test_microbench_umma.py)
   const int sms = pr.multiProcessorCount;
   for (int cps : {2, 3, 4}) bench<true, 2>(dU1, dU2, rows, 20, cps, 0, sms);
   for (int cps : {2, 3, 4}) bench<true, 3>(dU1, dU2, rows, 20, cps, 0, sms);
