@@ -69,7 +69,7 @@ class TuningC(C.Structure):
                 ("side_sampler_ctas", C.c_int32), ("heavy_per", C.c_int32),
                 ("heavy_win_log2", C.c_int32), ("heavy_big_log2", C.c_int32),
                 ("host_threads", C.c_int32), ("update_ctas_per_sm", C.c_int32), ("update_carveout", C.c_int32), ("graph", C.c_int32), ("peer_fence", C.c_int32),
-                ("nat_pad", C.c_int32), ("item_order", C.c_int32)]
+                ("nat_pad", C.c_int32), ("tiny_sampler", C.c_int32), ("item_order", C.c_int32)]
 
 
 OBSERVER = C.CFUNCTYPE(None, C.POINTER(MetricsRecordC), C.c_void_p, C.c_void_p)

@@ -738,6 +738,7 @@ int ntcb_set_tuning(ntcb_context* ctx, const ntcb_tuning* t) {
   if (t->nat_pad < -1 || t->nat_pad > 2) fail(NTCB_EINVAL, "tuning: nat_pad must be -1, 0, 1 or 2");
   if (t->peer_fence < 0 || t->peer_fence > 2) fail(NTCB_EINVAL, "tuning: peer_fence must be 0, 1 or 2");
   if (t->graph != 0 && t->graph != 1) fail(NTCB_EINVAL, "tuning: graph must be 0 or 1");
+  if (t->tiny_sampler != 0 && t->tiny_sampler != 1) fail(NTCB_EINVAL, "tuning: tiny_sampler must be 0 or 1");
   if (t->item_order != 0 && t->item_order != 1) fail(NTCB_EINVAL, "tuning: item_order must be 0 or 1");
   if (t->update_ctas_per_sm < 0) fail(NTCB_EINVAL, "tuning: update_ctas_per_sm must be >= 0");
   if (t->update_carveout < -1 || t->update_carveout > 100)

@@ -115,6 +115,7 @@ inline ntcb_tuning default_tuning() {
   t.peer_fence = 1;
   t.graph = 0;
   t.nat_pad = -1;
+  t.tiny_sampler = 1;
   t.item_order = 0;
   return t;
 }

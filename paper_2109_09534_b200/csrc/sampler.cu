@@ -53,6 +53,7 @@ struct SampleArgs {
   uint32_t mask_bytes;           // per-warp smem bytes for the slice bitmask
   uint32_t warp_bytes;           // per-warp total
   int direct;                    // 1: `root` is the row stream itself (sample_row)
+  uint32_t tiny_cap;             // slices up to this length are left to k_sample_tiny (0: none)
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -245,6 +246,55 @@ __device__ __forceinline__ void tmax(uint16_t* T, uint32_t r, uint32_t v) {
 }
 __device__ __forceinline__ void tmax(uint32_t* T, uint32_t r, uint32_t v) { atomicMax(T + r, v); }
 
+
+// Tiny slices (2 <= n <= kTinyCap): ONE LANE per slice runs the reference's
+// partial Fisher-Yates itself (nmc.cpp:44-63 with the exact next_below of
+// rng.hpp:32-45), its permutation in a 32-byte column of shared memory, and
+// ORs the picked set into the mask.  The Zipf tails of configs 3 and 5 are
+// millions of such slices (69 % of config 5's mode-0 rows): a warp per slice
+// spends a chain of phase latencies on a handful of draws.
+constexpr uint32_t kTinyCap = 32;
+constexpr uint64_t kTinyMin = 4096;  // tiny slices in a plan before the lane kernel is worth a launch
+__global__ void __launch_bounds__(256) k_sample_tiny(SampleArgs a) {
+  __shared__ unsigned char perm_s[kTinyCap * 256];  // [position][thread]
+  unsigned char* pm = perm_s + threadIdx.x;
+  for (uint64_t p = a.row_begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < a.row_end;
+       p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t beg = a.off[p];
+    const uint64_t n64 = a.off[p + 1] - beg;
+    if (n64 < 2 || n64 > kTinyCap) continue;
+    const uint32_t n = static_cast<uint32_t>(n64);
+    const uint32_t b = static_cast<uint32_t>(blocksize_for(a.c, n));
+    if (b == 0) continue;
+    for (uint32_t i = 0; i < n; ++i) pm[i * 256] = static_cast<unsigned char>(i);
+    uint64_t s = fork64(a.root, p);
+    uint32_t set = 0;
+    for (uint32_t j = 0; j < b; ++j) {
+      const uint64_t bd = n - j;
+      s += kGolden;
+      uint64_t x = mix64(s);
+      uint64_t lo = x * bd, hi = __umul64hi(x, bd);
+      if (lo < bd) {  // rng.hpp:36-43
+        const uint64_t th = (0 - bd) % bd;
+        while (lo < th) {
+          s += kGolden;
+          x = mix64(s);
+          lo = x * bd;
+          hi = __umul64hi(x, bd);
+        }
+      }
+      const uint32_t r = j + static_cast<uint32_t>(hi);
+      const unsigned char pj = pm[j * 256], pr = pm[r * 256];
+      pm[j * 256] = pr;
+      pm[r * 256] = pj;
+      set |= 1u << pr;  // the pick: perm[j] after the swap
+    }
+    const uint32_t sh = static_cast<uint32_t>(beg & 31u);
+    atomicOr(&a.mask[beg >> 5], set << sh);
+    if (sh && (set >> (32u - sh))) atomicOr(&a.mask[(beg >> 5) + 1], set >> (32u - sh));
+  }
+}
+
 template <typename TT>
 __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) {
   constexpr uint32_t FLAG = 1u << (8 * sizeof(TT) - 1);
@@ -260,7 +310,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
     const uint64_t beg = a.off[p];
     const uint32_t n = static_cast<uint32_t>(a.off[p + 1] - beg);
     const uint32_t b = static_cast<uint32_t>(blocksize_for(a.c, n));
-    if (b == 0 || a.c >= 1.0 || n > a.cap) continue;  // skipped / full / heavy slices
+    if (b == 0 || a.c >= 1.0 || n > a.cap || n <= a.tiny_cap) continue;  // skipped / full / heavy / tiny slices
     const uint64_t state0 = a.direct ? a.root : fork64(a.root, p);
     {
       const uint32_t pw = (n * static_cast<uint32_t>(sizeof(TT)) + 15) / 16;
@@ -543,6 +593,7 @@ struct SampleBucket {
 };
 struct SamplePlan {
   uint64_t n_short = 0;
+  uint64_t n_tiny = 0;  // of those, slices of at most kTinyCap entries
   SampleBucket mid[2];
 };
 using SamplePlans = std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, SamplePlan>;
@@ -558,6 +609,7 @@ static const SamplePlan& sample_plan(ntcb_context* ctx, const DeviceView& v, uin
   for (uint64_t p = r0; p < r1; ++p) {
     const uint64_t n = v.h_off[p + 1] - v.h_off[p];
     if (n < 2) continue;  // b = floor(c n) = 0 for c < 1
+    if (n <= kTinyCap) ++pl.n_tiny;
     if (n <= kWarpCap)
       ++pl.n_short;
     else if (n <= cap)
@@ -623,6 +675,16 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
     a.counters = ctx->counters;
     a.direct = direct;
     a.cap = std::min<uint64_t>(v.max_slice, kWarpCap);
+    // the Zipf tail: a lane per slice instead of a warp per slice
+    const bool tiny = !direct && ctx->tune.tiny_sampler != 0 && pl.n_tiny >= kTinyMin;
+    a.tiny_cap = tiny ? kTinyCap : 0u;
+    if (tiny) {
+      const uint64_t rows = row_end - row_begin;
+      const uint64_t tg = std::min<uint64_t>((rows + 255) / 256, static_cast<uint64_t>(ctx->sm_count) * 8);
+      k_sample_tiny<<<static_cast<unsigned>(tg), 256, 0, stream>>>(a);
+      NTCB_CUDA(cudaGetLastError());
+      ++launches;
+    }
     a.warp_bytes = static_cast<uint32_t>((a.cap * 2 + 15) / 16 * 16);
     const size_t smem = static_cast<size_t>(a.warp_bytes) * kSampleWarps;
     int per_sm = 0;
