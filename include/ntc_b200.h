@@ -133,7 +133,7 @@ typedef struct ntcb_tuning {
                                 reference); 1 on, 0 off, -1 (default) when the factors exceed 16 MB
                                 (gathers mostly miss L1: configs 3 and 5 measured 2.6 % / 5 % faster,
                                 configs 1 and 2, whose factors stay cached, slower) */
-  int32_t tiny_sampler;      /* 1 (default): slices of at most 32 entries are sampled by one lane each
+  int32_t tiny_sampler;      /* 1 (default): slices of at most 64 entries are sampled by one lane each
                                 (k_sample_tiny) when a mode has thousands of them; 0: a warp per slice */
   int32_t item_order;        /* work-list order of equally long update items: 0 row-major (a row's chunks
                                 together), 1 chunk-major (chunk s of every row together: co-resident

@@ -54,6 +54,7 @@ struct SampleArgs {
   uint32_t warp_bytes;           // per-warp total
   int direct;                    // 1: `root` is the row stream itself (sample_row)
   uint32_t tiny_cap;             // slices up to this length are left to k_sample_tiny (0: none)
+  uint32_t scan_w;               // k_sample_set: consecutive rows a warp examines at once (1..32)
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -253,7 +254,10 @@ __device__ __forceinline__ void tmax(uint32_t* T, uint32_t r, uint32_t v) { atom
 // ORs the picked set into the mask.  The Zipf tails of configs 3 and 5 are
 // millions of such slices (69 % of config 5's mode-0 rows): a warp per slice
 // spends a chain of phase latencies on a handful of draws.
-constexpr uint32_t kTinyCap = 32;
+#ifndef NTCB_TINY_CAP
+#define NTCB_TINY_CAP 64
+#endif
+constexpr uint32_t kTinyCap = NTCB_TINY_CAP;  // 32 or 64
 constexpr uint64_t kTinyMin = 4096;  // tiny slices in a plan before the lane kernel is worth a launch
 __global__ void __launch_bounds__(256) k_sample_tiny(SampleArgs a) {
   __shared__ unsigned char perm_s[kTinyCap * 256];  // [position][thread]
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(256) k_sample_tiny(SampleArgs a) {
     if (b == 0) continue;
     for (uint32_t i = 0; i < n; ++i) pm[i * 256] = static_cast<unsigned char>(i);
     uint64_t s = fork64(a.root, p);
-    uint32_t set = 0;
+    uint64_t set = 0;
     for (uint32_t j = 0; j < b; ++j) {
       const uint64_t bd = n - j;
       s += kGolden;
@@ -287,11 +291,20 @@ __global__ void __launch_bounds__(256) k_sample_tiny(SampleArgs a) {
       const unsigned char pj = pm[j * 256], pr = pm[r * 256];
       pm[j * 256] = pr;
       pm[r * 256] = pj;
-      set |= 1u << pr;  // the pick: perm[j] after the swap
+      set |= 1ull << pr;  // the pick: perm[j] after the swap
     }
+    // the set's bits at absolute entry positions beg .. beg + n - 1 (up to three mask words)
     const uint32_t sh = static_cast<uint32_t>(beg & 31u);
-    atomicOr(&a.mask[beg >> 5], set << sh);
-    if (sh && (set >> (32u - sh))) atomicOr(&a.mask[(beg >> 5) + 1], set >> (32u - sh));
+    const uint32_t w0 = static_cast<uint32_t>(set << sh);
+    const uint64_t rest = sh ? set >> (32u - sh) : set >> 32;  // bits from word 1 on
+    uint32_t* m = a.mask + (beg >> 5);
+    if (w0) atomicOr(m, w0);
+    if (sh) {
+      if (static_cast<uint32_t>(rest)) atomicOr(m + 1, static_cast<uint32_t>(rest));
+      if (rest >> 32) atomicOr(m + 2, static_cast<uint32_t>(rest >> 32));
+    } else if (static_cast<uint32_t>(rest)) {
+      atomicOr(m + 1, static_cast<uint32_t>(rest));
+    }
   }
 }
 
@@ -306,11 +319,30 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
   if (*reinterpret_cast<volatile unsigned long long*>(&a.counters[1]) != ~0ull) return;
   const uint64_t lane_off = static_cast<uint64_t>(lane + 1) * kGolden;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kSampleWarps;
-  for (uint64_t p = a.row_begin + blockIdx.x * kSampleWarps + wib; p < a.row_end; p += nw) {
-    const uint64_t beg = a.off[p];
-    const uint32_t n = static_cast<uint32_t>(a.off[p + 1] - beg);
-    const uint32_t b = static_cast<uint32_t>(blocksize_for(a.c, n));
-    if (b == 0 || a.c >= 1.0 || n > a.cap || n <= a.tiny_cap) continue;  // skipped / full / heavy / tiny slices
+  // The warp examines scan_w consecutive rows at once (one coalesced read of
+  // their offsets) and then samples the ones of its class one by one: with a
+  // Zipf tail most rows belong to k_sample_tiny, and skipping them one
+  // dependent offset load at a time was most of this kernel's time.
+  const uint32_t sw = a.scan_w;
+  for (uint64_t base = a.row_begin + (blockIdx.x * static_cast<uint64_t>(kSampleWarps) + wib) * sw; base < a.row_end;
+       base += nw * sw) {
+   const uint64_t pl = base + lane;
+   uint64_t beg_l = 0;
+   uint32_t n_l = 0;
+   if (static_cast<uint32_t>(lane) < sw && pl < a.row_end) {
+     beg_l = a.off[pl];
+     n_l = static_cast<uint32_t>(a.off[pl + 1] - beg_l);
+   }
+   const uint32_t b_l = static_cast<uint32_t>(blocksize_for(a.c, n_l));
+   // skipped / full / heavy / tiny slices are not this kernel's
+   uint32_t todo = __ballot_sync(kFull, !(b_l == 0 || a.c >= 1.0 || n_l > a.cap || n_l <= a.tiny_cap));
+   while (todo) {
+    const int tq = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint64_t p = base + tq;
+    const uint64_t beg = __shfl_sync(kFull, beg_l, tq);
+    const uint32_t n = __shfl_sync(kFull, n_l, tq);
+    const uint32_t b = __shfl_sync(kFull, b_l, tq);
     const uint64_t state0 = a.direct ? a.root : fork64(a.root, p);
     {
       const uint32_t pw = (n * static_cast<uint32_t>(sizeof(TT)) + 15) / 16;
@@ -420,6 +452,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample_set(SampleArgs a) 
       }
     }
     __syncwarp();
+   }
   }
 }
 
@@ -691,7 +724,11 @@ int launch_sample_set(ntcb_context* ctx, cudaStream_t stream, uint32_t* mask, in
     NTCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_set<uint16_t>,
                                                             kSampleWarps * 32, smem));
     if (per_sm < 1) per_sm = 1;
-    uint64_t grid = (row_end - row_begin + kSampleWarps - 1) / kSampleWarps;
+    // rows examined per warp step: as wide as leaves every resident warp at least four steps
+    const uint64_t resident = static_cast<uint64_t>(per_sm) * ctx->sm_count * kSampleWarps;
+    a.scan_w = 1;
+    while (a.scan_w < 32 && (row_end - row_begin) / (2ull * a.scan_w) >= 4 * resident) a.scan_w *= 2;
+    uint64_t grid = ((row_end - row_begin + a.scan_w - 1) / a.scan_w + kSampleWarps - 1) / kSampleWarps;
     grid = std::min<uint64_t>(grid, static_cast<uint64_t>(per_sm) * ctx->sm_count);
     k_sample_set<uint16_t><<<static_cast<unsigned>(grid), kSampleWarps * 32, smem, stream>>>(a);
     NTCB_CUDA(cudaGetLastError());
