@@ -295,11 +295,14 @@ def cpu_baseline_sample(cfgd, cid):
 
 # ---------------------------------------------------------------------------
 def roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches, smp_ms_step,
-                   upd_ms_step):
-    """Roofline of the dominant kernel (one mode update: k_update_tc + the
-    split-row finalisation), SURVEY.md §8(d).
+                   upd_ms_step, kern=None):
+    """Roofline of the dominant kernel (the update's item kernel, k_update_tc),
+    SURVEY.md §8(d).
     achieved = algorithmic bytes per launch / this run's average launch time
-    (CUDA events on the library stream), against the measured HBM peak.
+    of THAT kernel (CUDA events on the library stream right before and after
+    it, ntcb_profile_read_kernel), against the measured HBM peak; the span of
+    a whole mode update (item kernel + split-row finalisation kernels) is
+    reported beside it as update_span_ms.
     Algorithmic bytes = 4N B per sampled entry (value + N-1 coordinates) +
     (16R + 8) B per processed row; factor-row gathers are NOT counted (they
     are L1/L2 traffic at configs 1-4; at config 5 they partly reach DRAM and
@@ -315,7 +318,8 @@ def roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_
     alg_bytes = 4 * N * full + (16 * R + 8) * rows_processed  # per sweep
     gathers = (N - 1) * 4 * R * full
     per_launch = alg_bytes / N
-    avg_s = (upd_ms / max(upd_launches, 1)) / 1000.0
+    span_s = (upd_ms / max(upd_launches, 1)) / 1000.0
+    avg_s = (kern[0] / kern[1] / 1000.0) if kern and kern[1] else span_s
     achieved = per_launch / avg_s / 1e9
     alg_flops = 2 * ((N - 2) * R + 3 * R + R * (R + 1) // 2) * full + 8 * R * rows_processed
     flops_launch = alg_flops / N
@@ -325,7 +329,7 @@ def roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_
            "kernel": update_kernel_name(R, N, ctx.factor_device_ptr(0)[1]),
            "alg_bytes_per_launch": per_launch,
            "gather_bytes_if_uncached_per_launch": gathers / N,
-           "avg_launch_ms": avg_s * 1000.0,
+           "avg_launch_ms": avg_s * 1000.0, "update_span_ms": span_s * 1000.0,
            # side-stream spans include queueing behind the update: not busy time
            "sampler_span_ms_per_step": smp_ms_step, "update_ms_per_step": upd_ms_step,
            "compute": {"alg_flops_per_launch": flops_launch, "achieved_tflops": flops_launch / avg_s / 1e12,
@@ -384,6 +388,7 @@ def sub_record(cid, steps=3, warmup=3, tune=()):
         for k in range(warmup, warmup + steps):
             ctx.sweep_async(k, cfg, SEED_SOLVER)
         ctx.collect()
+        kern = ctx.profile_read_kernel()
         upd_ms, smp_ms, launches, upd_launches = ctx.profile_read()
         ctx.profile(False)
         e2e = e2e_host(ctx, dims, cfg, steps, P)
@@ -392,7 +397,7 @@ def sub_record(cid, steps=3, warmup=3, tune=()):
                 "warmup": warmup, "sampled_per_ao_iteration": full, "l2": l2_note(cfgd),
                 "e2e": e2e, "gpu_launches": launches,
                 "roofline": roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches,
-                                           smp_ms / steps, upd_ms / steps)}
+                                           smp_ms / steps, upd_ms / steps, kern)}
     finally:
         ctx.close()
 
@@ -508,6 +513,7 @@ def run_ours(args, cfgd, cid):
     for k in range(args.warmup, args.warmup + args.steps):
         step(k)
     ctx.collect()
+    kern = ctx.profile_read_kernel()
     upd_ms, smp_ms, launches, upd_launches = ctx.profile_read()
     ctx.profile(False)
     # soak: keep the GPU loaded a little longer so the clock sampler sees it
@@ -528,7 +534,7 @@ def run_ours(args, cfgd, cid):
     value = total_sampled / (ms / 1000.0)
 
     roofline = roofline_block(ctx, cfgd, cid, offs, cfg, full, rows_processed, upd_ms, upd_launches,
-                              smp_ms / args.steps, upd_ms / args.steps)
+                              smp_ms / args.steps, upd_ms / args.steps, kern)
 
     # ---- end to end through the host-buffer C-ABI --------------------------------
     e2e = None

@@ -350,6 +350,10 @@ int ntcb_synth(ntcb_context* ctx, int order, const uint64_t* dims, uint64_t nnz,
  * (side stream), the number of kernel launches issued, and the number of
  * timed mode updates (update_launches; at most 2048 phases are timed). */
 int ntcb_profile_enable(ntcb_context* ctx, int on);
+/* The update's item kernel alone (gradient + Hessian + row end of unsplit rows; without the
+ * split-row finalisation kernels): summed device time and launch count since profiling was
+ * enabled or last read. */
+int ntcb_profile_read_kernel(ntcb_context* ctx, double* item_kernel_ms, uint64_t* launches);
 int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms,
                       uint64_t* launches, uint64_t* update_launches);
 

@@ -147,6 +147,7 @@ SIGNATURES = {
     "ntcb_render_model": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8)]),
     "ntcb_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "ntcb_profile_read": (C.c_int, [C.c_void_p, f64p, f64p, u64p, u64p]),
+    "ntcb_profile_read_kernel": (C.c_int, [C.c_void_p, f64p, u64p]),
 }
 
 _L = None

@@ -670,6 +670,7 @@ int ntcb_create(int device, ntcb_context** out) {
   const unsigned long long init[8] = {0, ~0ull, 0, 0, 0, 0, 0, 0};
   NTCB_CUDA(cudaMemcpy(ctx->counters, init, sizeof init, cudaMemcpyHostToDevice));
   for (auto& e : ctx->prof.ev) NTCB_CUDA(cudaEventCreate(&e));
+  for (auto& e : ctx->prof.kev) NTCB_CUDA(cudaEventCreate(&e));
   ctx->host = new HostState();
   *out = ctx;
   API_CATCH
@@ -686,6 +687,7 @@ int ntcb_destroy(ntcb_context* ctx) {
   cudaFree(ctx->counters);
   cudaFreeHost(ctx->h_counters);
   for (auto& e : ctx->prof.ev) cudaEventDestroy(e);
+  for (auto& e : ctx->prof.kev) cudaEventDestroy(e);
   for (auto& mm : ctx->ev_sampled)
     for (auto& e : mm) cudaEventDestroy(e);
   for (auto& mm : ctx->ev_consumed)
@@ -1591,6 +1593,7 @@ int ntcb_profile_enable(ntcb_context* ctx, int on) {
   need_ctx(ctx);
   ctx->prof.on = on != 0;
   ctx->prof.n = 0;
+  ctx->prof.kn = 0;
   ctx->prof.launches = 0;
   ctx->prof.update_launches = 0;
   API_CATCH
@@ -1622,6 +1625,25 @@ int ntcb_profile_read(ntcb_context* ctx, double* update_ms, double* sample_ms, u
   pf.n = 0;
   pf.launches = 0;
   pf.update_launches = 0;
+  API_CATCH
+}
+
+int ntcb_profile_read_kernel(ntcb_context* ctx, double* item_kernel_ms, uint64_t* launches) {
+  API_TRY
+  need_ctx(ctx);
+  NTCB_CUDA(cudaStreamSynchronize(ctx->stream));
+  Profile& pf = ctx->prof;
+  double t = 0.0;
+  uint64_t n = 0;
+  for (int i = 0; i + 1 < pf.kn; i += 2) {
+    float ms = 0.f;
+    NTCB_CUDA(cudaEventElapsedTime(&ms, pf.kev[i], pf.kev[i + 1]));
+    t += ms;
+    ++n;
+  }
+  if (item_kernel_ms) *item_kernel_ms = t;
+  if (launches) *launches = n;
+  pf.kn = 0;
   API_CATCH
 }
 

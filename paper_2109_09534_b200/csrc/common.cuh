@@ -96,6 +96,9 @@ struct Profile {
   int n = 0;
   uint64_t launches = 0;
   uint64_t update_launches = 0;
+  // the item kernel alone (k_update_tc / k_update, without the split-row finalisation): start/end pairs
+  cudaEvent_t kev[1024];
+  int kn = 0;
 };
 
 inline ntcb_tuning default_tuning() {
@@ -180,6 +183,12 @@ struct ntcb_context {
 };
 
 namespace ntcb {
+// Profiling: an event on the library stream before / after the update's item kernel.
+inline void prof_kernel_mark(ntcb_context* ctx) {
+  Profile& pf = ctx->prof;
+  if (!pf.on || pf.kn >= 1024) return;
+  cudaEventRecord(pf.kev[pf.kn++], ctx->stream);
+}
 // The per-entry sampler scratch, indexed by absolute view position of `mode`.
 inline uint32_t* view_scratch(ntcb_context* ctx, int mode) {
   return ctx->perm_scratch ? ctx->perm_scratch - ctx->views[mode].a_lo : nullptr;

@@ -1826,6 +1826,7 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
   // view (a property of the mode, not of a shard: the instantiation must not
   // depend on the partition) -- per-row latencies dominate there
   const bool short_rows = mode_short_rows(ctx, a.mode, a.c);
+  if (pl.n_items) prof_kernel_mark(ctx);
   if (pl.n_items && !g_tc_off && !nat_off && a.ld == 16 && ctx->nat_padded && a.rank <= 16 &&
       (a.no == 2 || a.no == 3)) {
     // ranks 9-16 on 64-byte rows: NAT with four lanes per pick
@@ -1868,6 +1869,7 @@ static int launch_ld(ntcb_context* ctx, UpdateArgs& a, const WorkPlan& pl) {
     else
       launches += launch_items<LD4, NTCB_MAX_ORDER - 1>(ctx, a, pl, smem);
   }
+  if (pl.n_items) prof_kernel_mark(ctx);
   launches += launch_finalize_ld<LD4>(ctx, a, pl);
   return launches;
 }

@@ -525,6 +525,12 @@ class Context:
     def profile(self, on=True):
         check(self.L.ntcb_profile_enable(self.h, int(on)))
 
+    def profile_read_kernel(self):
+        """(ms, launches) of the update's item kernel alone since profiling was enabled."""
+        t, n = C.c_double(), C.c_uint64()
+        check(self.L.ntcb_profile_read_kernel(self.h, C.byref(t), C.byref(n)))
+        return t.value, n.value
+
     def profile_read(self):
         u, s = C.c_double(), C.c_double()
         n, nu = C.c_uint64(), C.c_uint64()
